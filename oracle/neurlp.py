@@ -1,0 +1,366 @@
+"""Plain float64 CPU oracle of the NeuRLP-PDE solve (arXiv 2502.18377, §3).
+
+TEST INFRASTRUCTURE ONLY -- see ``oracle/__init__.py``.  Nothing here is blocked,
+fused or reordered beyond what the paper's definitions state: the constraint
+matrix A and vector d are assembled explicitly row by row (Eqs. 3-8), the least
+squares problem is solved through its normal equations (Eq. 9), the duals are the
+first block row of the saddle system (Eq. 10) and the backward pass is Eq. 11
+followed by the gradient formulas of P:240.
+
+Conventions:
+  * points are row-major with dim 0 = time slowest; variables are field-major
+    z[m*P + p] with fields ordered (phi, d0, d00, d1, d11, ...)             (Q2)
+  * the boundary set B is every point on any face of the space-time box       (Q1)
+  * derivative rows: h_d^k z[(d,k),p] - sum_j a^k_j z[phi, p + o_j e_d] = 0
+    with 5-point central weights for 2 <= i_d <= n_d-3 and fully one-sided
+    5-point weights at the two points nearest each edge                 (Q4, Q5)
+  * smoothness rows in both directions wherever the neighbour exists         (Q7)
+  * duals lambda = d - A z                                                   (Q8)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+
+# ----------------------------------------------------------------------------
+# Problem description
+# ----------------------------------------------------------------------------
+@dataclass(frozen=True)
+class Problem:
+    """One grid + weights.  P:89 (§2 Cartesian grid), P:114-117 (uniform steps).
+
+    ``shape`` = points per dim (dim 0 = t), ``h`` = step per dim, weights are the
+    row-group weights (Q6; the paper's Eqs. 8-9 are unweighted = all 1).
+    """
+    shape: tuple
+    h: tuple
+    w_eq: float = 1.0
+    w_bnd: float = 1.0
+    w_der: float = 1.0
+    w_sm: float = 1.0
+
+    @property
+    def D(self) -> int:
+        return len(self.shape)
+
+    @property
+    def P(self) -> int:
+        return int(np.prod(self.shape))
+
+    @property
+    def M(self) -> int:
+        return n_fields(self.D)
+
+    @property
+    def n_v(self) -> int:
+        return self.M * self.P
+
+
+def n_fields(D: int) -> int:
+    """|M| = 1 + 2D: phi plus first and second pure derivative per dim (Q2)."""
+    return 1 + 2 * D
+
+
+def field_index(d: int, k: int) -> int:
+    """Index of the field holding the k-th derivative (k = 1, 2) along dim d."""
+    return 1 + 2 * d + (k - 1)
+
+
+def boundary_mask(shape) -> np.ndarray:
+    """B = points with i_d in {0, n_d-1} for some d (reading Q1)."""
+    mask = np.zeros(shape, dtype=bool)
+    for d, n in enumerate(shape):
+        sl = [slice(None)] * len(shape)
+        sl[d] = 0
+        mask[tuple(sl)] = True
+        sl[d] = n - 1
+        mask[tuple(sl)] = True
+    return mask.reshape(-1)
+
+
+# 5-point finite-difference weights on a unit-spaced grid ("5 point central
+# differences and ... forward, backward finite differences at the edges").
+_A_CENTRAL = {1: np.array([1.0, -8.0, 0.0, 8.0, -1.0]) / 12.0,
+              2: np.array([-1.0, 16.0, -30.0, 16.0, -1.0]) / 12.0}
+_A_FORWARD = {1: np.array([-25.0, 48.0, -36.0, 16.0, -3.0]) / 12.0,
+              2: np.array([35.0, -104.0, 114.0, -56.0, 11.0]) / 12.0}
+
+
+def fd_stencil(k: int, i: int, n: int):
+    """(offsets, weights) of the k-th derivative stencil at index i of an n-point axis.
+
+    Central for 2 <= i <= n-3, forward (offsets 0..4) for i < 2, backward
+    (offsets 0..-4, a_bwd(-j) = (-1)^k a_fwd(j)) for i > n-3.  P:169-174 (Eq. 5);
+    edge width/order is reading Q4.
+    """
+    if n < 6:
+        raise ValueError("each dim needs >= 6 points for the 5-point edge stencils (Q4)")
+    if 2 <= i <= n - 3:
+        return np.arange(-2, 3), _A_CENTRAL[k]
+    if i < 2:
+        return np.arange(0, 5), _A_FORWARD[k]
+    return -np.arange(0, 5), ((-1.0) ** k) * _A_FORWARD[k]
+
+
+def counts(shape):
+    """(n_v, n_c) of the constraint system, counted row group by row group.
+
+    n_c = P (Eq. 3) + |B| (Eq. 4) + 2D P (Eq. 5, one row per derivative variable)
+          + sum_d 2 (n_d - 1) P / n_d (Eqs. 6-7 where the neighbour exists).
+    """
+    D = len(shape)
+    P = int(np.prod(shape))
+    nb = int(boundary_mask(shape).sum())
+    smooth = sum(2 * (n - 1) * (P // n) for n in shape)
+    return n_fields(D) * P, P + nb + 2 * D * P + smooth
+
+
+# ----------------------------------------------------------------------------
+# Assembly: Eqs. 3-8
+# ----------------------------------------------------------------------------
+def assemble(prob: Problem, c: np.ndarray, b: np.ndarray, omega: np.ndarray):
+    """Explicit sparse A (n_c x n_v, CSR, fp64) and d for one PDE.  P:186-191 (Eq. 8).
+
+    c: [M][P] coefficient fields (Eq. 1); b: [P] right-hand side; omega: [P]
+    (only entries on B are read, Eq. 4).  Rows, in order:
+      equation rows  (Eq. 3)      w_eq * sum_m c_m[p] z[m,p]       = w_eq b[p]
+      boundary rows  (Eq. 4)      w_bnd * z[phi,p]                 = w_bnd omega[p]
+      derivative rows(Eq. 5)  w_der*(h^k z[(d,k),p] - sum_j a_j z[phi,p+o_j e_d]) = 0
+      smoothness rows(Eqs. 6-7)
+                      w_sm*(z[phi,p] +- h z[(d,1),p] + h^2/2 z[(d,2),p] - z[phi,p +- e_d]) = 0
+    Returns (A, d, info) with info = {eq_rows, bnd_points, bnd_rows}.
+    """
+    shape, D, P, M = tuple(prob.shape), prob.D, prob.P, prob.M
+    c = np.asarray(c, dtype=np.float64).reshape(M, P)
+    b = np.asarray(b, dtype=np.float64).reshape(P)
+    omega = np.asarray(omega, dtype=np.float64).reshape(P)
+    for n in shape:
+        if n < 6:
+            raise ValueError("each dim needs >= 6 points (Q4)")
+    pts = np.arange(P)
+    idx = np.unravel_index(pts, shape)
+    strides = [int(np.prod(shape[d + 1:])) for d in range(D)]
+    rows, cols, vals, dvec = [], [], [], []
+    r0 = 0
+
+    # Equation rows (Eq. 3).  Structural entries are kept even where c_m[p] = 0,
+    # because c is a parameter and its gradient lives on these entries.
+    for m in range(M):
+        rows.append(r0 + pts)
+        cols.append(m * P + pts)
+        vals.append(prob.w_eq * c[m])
+    dvec.append(prob.w_eq * b)
+    eq_rows = r0 + pts
+    r0 += P
+
+    # Boundary rows (Eq. 4): Dirichlet on u_phi.
+    bpts = np.flatnonzero(boundary_mask(shape))
+    rows.append(r0 + np.arange(bpts.size))
+    cols.append(0 * P + bpts)
+    vals.append(np.full(bpts.size, prob.w_bnd))
+    dvec.append(prob.w_bnd * omega[bpts])
+    bnd_rows = r0 + np.arange(bpts.size)
+    r0 += bpts.size
+
+    # Derivative rows (Eq. 5), one per (d, k, p).
+    for d in range(D):
+        n, hd, i_d = shape[d], prob.h[d], idx[d]
+        for k in (1, 2):
+            f = field_index(d, k)
+            rows.append(r0 + pts)
+            cols.append(f * P + pts)
+            vals.append(np.full(P, prob.w_der * hd ** k))
+            for i in range(n):
+                sel = pts[i_d == i]
+                offs, wts = fd_stencil(k, i, n)
+                for o, a in zip(offs, wts):
+                    if a == 0.0:
+                        continue
+                    rows.append(r0 + sel)
+                    cols.append(0 * P + sel + o * strides[d])
+                    vals.append(np.full(sel.size, -prob.w_der * a))
+            dvec.append(np.zeros(P))
+            r0 += P
+
+    # Smoothness rows (Eqs. 6-7), forward then backward, where the neighbour exists.
+    for d in range(D):
+        n, hd, i_d = shape[d], prob.h[d], idx[d]
+        f1, f2 = field_index(d, 1), field_index(d, 2)
+        for sgn in (+1, -1):
+            sel = pts[(i_d <= n - 2) if sgn > 0 else (i_d >= 1)]
+            rr = r0 + np.arange(sel.size)
+            w = prob.w_sm
+            for col, val in ((0 * P + sel, w), (f1 * P + sel, sgn * w * hd),
+                             (f2 * P + sel, 0.5 * w * hd * hd),
+                             (0 * P + sel + sgn * strides[d], -w)):
+                rows.append(rr)
+                cols.append(col)
+                vals.append(np.full(sel.size, val) if np.isscalar(val) else val)
+            dvec.append(np.zeros(sel.size))
+            r0 += sel.size
+
+    A = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(r0, M * P))
+    d_out = np.concatenate(dvec)
+    return A, d_out, {"eq_rows": eq_rows, "bnd_points": bpts, "bnd_rows": bnd_rows}
+
+
+def normal_apply(A: sp.csr_matrix, x: np.ndarray) -> np.ndarray:
+    """A^T (A x): the normal operator of Eq. 9 applied to x."""
+    return A.T @ (A @ x)
+
+
+# ----------------------------------------------------------------------------
+# Least squares on an arbitrary A: Eqs. 9-11 and P:240
+# ----------------------------------------------------------------------------
+def _svd_normal_solve(A, rhs):
+    """(A^T A)^{-1} rhs via the SVD A = U S V^T: V S^-2 V^T rhs (plain definition)."""
+    Ad = A.toarray() if sp.issparse(A) else np.asarray(A, dtype=np.float64)
+    _, s, vt = np.linalg.svd(Ad, full_matrices=False)
+    if s[-1] <= s[0] * 1e-13:
+        raise np.linalg.LinAlgError("A is column-rank-deficient (P:109 assumes uniqueness)")
+    return vt.T @ ((vt @ rhs) / (s * s))
+
+
+def _equilibration(N):
+    """S = diag(A^T A)^(-1/2): column equilibration (a change of variables)."""
+    dg = N.diagonal()
+    if np.any(dg <= 0):
+        raise np.linalg.LinAlgError("zero column in A")
+    return 1.0 / np.sqrt(dg)
+
+
+def solve_normal(A, rhs, method: str = "auto", tol: float = 1e-12, maxiter: int = 200000,
+                 info: dict | None = None):
+    """Solve A^T A x = rhs (Eq. 9).
+
+    method: 'dense' (SVD), 'lu' (SuperLU on S A^T A S + 2 fp64 refinement steps with
+    r = rhs - A^T A x) or 'cg' (textbook CG on S A^T A S, i.e. Jacobi-preconditioned
+    CG, stopping at ||rhs - A^T A x|| / ||rhs|| <= tol, true residual every 500 its).
+    """
+    n_v = A.shape[1]
+    if method == "auto":
+        method = "dense" if n_v <= 5000 else "cg"
+    info = {} if info is None else info
+    info["method"] = method
+    rhs = np.asarray(rhs, dtype=np.float64)
+    if not np.any(rhs):
+        info["iters"] = 0
+        return np.zeros(n_v)
+    if method == "dense":
+        return _svd_normal_solve(A, rhs)
+    N = (A.T @ A).tocsr()
+    s = _equilibration(N)
+    if method == "lu":
+        Ns = sp.diags(s) @ N @ sp.diags(s)
+        lu = spla.splu(Ns.tocsc())
+        x = s * lu.solve(s * rhs)
+        for _ in range(2):
+            r = rhs - N @ x
+            x = x + s * lu.solve(s * r)
+        return x
+    if method == "cg":
+        minv = s * s
+        x = np.zeros(n_v)
+        r = rhs.copy()
+        zv = minv * r
+        p = zv.copy()
+        rz = r @ zv
+        nrm = np.linalg.norm(rhs)
+        it = 0
+        while it < maxiter:
+            q = N @ p
+            alpha = rz / (p @ q)
+            x += alpha * p
+            r -= alpha * q
+            it += 1
+            if it % 500 == 0:
+                r = rhs - N @ x
+            if np.linalg.norm(r) <= tol * nrm:
+                r = rhs - N @ x
+                if np.linalg.norm(r) <= tol * nrm:
+                    break
+            zv = minv * r
+            rz_new = r @ zv
+            p = zv + (rz_new / rz) * p
+            rz = rz_new
+        info["iters"] = it
+        info["rel_res"] = float(np.linalg.norm(rhs - N @ x) / nrm)
+        return x
+    raise ValueError(method)
+
+
+def lstsq_forward(A, d, method: str = "auto", tol: float = 1e-12, info=None):
+    """Forward pass: z* from A^T A z = A^T d (Eq. 9); lambda* = d - A z* (Eq. 10
+    first block row, reading Q8).  'dense' solves min ||Az - d|| by SVD directly."""
+    d = np.asarray(d, dtype=np.float64)
+    if method == "dense" or (method == "auto" and A.shape[1] <= 5000):
+        Ad = A.toarray() if sp.issparse(A) else np.asarray(A, dtype=np.float64)
+        z = np.linalg.lstsq(Ad, d, rcond=None)[0]
+        if info is not None:
+            info["method"] = "dense"
+    else:
+        z = solve_normal(A, A.T @ d, method=method, tol=tol, info=info)
+    lam = d - A @ z
+    return z, lam
+
+
+def lstsq_backward(A, z, lam, g, method: str = "auto", tol: float = 1e-12, info=None):
+    """Backward pass (Eq. 11).
+
+    [[I, A], [A^T, 0]] [d_lam; d_z] = [0; -g]  =>  A^T A d_z = g,  d_lam = -A d_z.
+    dA = d_lam z*^T + lambda* d_z^T on A's pattern, dd = -d_lam.
+    Returns (d_z, d_lam, dA as a sparse matrix on A's pattern, dd).
+    """
+    dz = solve_normal(A, g, method=method, tol=tol, info=info)
+    dlam = -(A @ dz)
+    Acoo = sp.coo_matrix(A)
+    gv = dlam[Acoo.row] * z[Acoo.col] + lam[Acoo.row] * dz[Acoo.col]
+    dA = sp.csr_matrix((gv, (Acoo.row, Acoo.col)), shape=A.shape)
+    return dz, dlam, dA, -dlam
+
+
+# ----------------------------------------------------------------------------
+# PDE-level forward / backward
+# ----------------------------------------------------------------------------
+def solve_forward(prob: Problem, c, b, omega, method: str = "auto", tol: float = 1e-12):
+    """Forward NeuRLP-PDE solve of one PDE.  Returns dict(z, lam, A, d, info)."""
+    A, d, info = assemble(prob, c, b, omega)
+    sinfo = {}
+    z, lam = lstsq_forward(A, d, method=method, tol=tol, info=sinfo)
+    info.update(solve=sinfo)
+    return {"z": z, "lam": lam, "A": A, "d": d, "info": info}
+
+
+def field_gradients(prob: Problem, info, z, lam, dz, dlam):
+    """Chain dA, dd through the assembly of Eqs. 3-4 to the encoder outputs.
+
+    A[eq(p), (m,p)] = w_eq c_m[p]    =>  dl/dc_m[p] = w_eq * dA[eq(p), (m,p)]
+    d[eq(p)]        = w_eq b[p]      =>  dl/db[p]   = w_eq * dd[eq(p)]
+    d[bnd(p)]       = w_bnd omega[p] =>  dl/domega[p] = w_bnd * dd[bnd(p)], 0 off B
+    with dA[i,j] = d_lam[i] z[j] + lam[i] d_z[j] and dd = -d_lam evaluated at the entries.
+    """
+    P, M = prob.P, prob.M
+    er = info["eq_rows"]
+    grad_c = np.empty((M, P))
+    for m in range(M):
+        j = m * P + np.arange(P)
+        grad_c[m] = prob.w_eq * (dlam[er] * z[j] + lam[er] * dz[j])
+    grad_b = prob.w_eq * (-dlam[er])
+    grad_omega = np.zeros(P)
+    grad_omega[info["bnd_points"]] = prob.w_bnd * (-dlam[info["bnd_rows"]])
+    return grad_c, grad_b, grad_omega
+
+
+def solve_backward(prob: Problem, fwd: dict, g, method: str = "auto", tol: float = 1e-12):
+    """Backward NeuRLP-PDE solve for g = dl/dz* (Eq. 11) and field gradients."""
+    sinfo = {}
+    dz, dlam, dA, dd = lstsq_backward(fwd["A"], fwd["z"], fwd["lam"], g, method=method,
+                                      tol=tol, info=sinfo)
+    gc, gb, gw = field_gradients(prob, fwd["info"], fwd["z"], fwd["lam"], dz, dlam)
+    return {"dz": dz, "dlam": dlam, "dA": dA, "dd": dd, "grad_c": gc, "grad_b": gb,
+            "grad_omega": gw, "info": sinfo}

@@ -1,0 +1,350 @@
+"""Pins of the CPU float64 oracle against what the paper and mathematics fix.
+
+Each test names the passage or closed form it pins.  None of
+these compares the oracle with itself: values come from PAPER.md (tests/golden/),
+closed forms, or invariants a dropped term / wrong sign / transposed operand breaks.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import (Problem, assemble, boundary_mask, counts, fd_stencil, field_index,
+                    lstsq_backward, lstsq_forward, normal_apply, solve_backward,
+                    solve_forward)
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _coords(shape, h):
+    axes = [np.arange(n) * hh for n, hh in zip(shape, h)]
+    return np.meshgrid(*axes, indexing="ij")
+
+
+def _rand_c(shape, rng):
+    D = len(shape)
+    c = rng.normal(0.0, 0.5, (1 + 2 * D,) + tuple(shape))
+    c[1] += 1.0  # keep u_t present (well-posed evolution problems)
+    return c.reshape(1 + 2 * D, -1)
+
+
+# --------------------------------------------------------------------- P1 counts
+def test_paper_counts_32x32():
+    """P:244 'for a PDE defined over 32x32 grids we have 5120 variables and 9212
+    constraints, requiring 377 MB of double precision dense storage' and P:249 99.9%."""
+    g = json.load(open(os.path.join(GOLD, "paper_counts.json")))["32x32"]
+    pr = Problem((32, 32), (1 / 31, 1 / 31))
+    rng = np.random.default_rng(0)
+    A, d, _ = assemble(pr, _rand_c((32, 32), rng), np.zeros(1024), np.zeros(1024))
+    assert A.shape == (g["n_c"], g["n_v"])
+    assert counts((32, 32)) == (g["n_v"], g["n_c"])
+    assert round(A.shape[0] * A.shape[1] * 8 / 1e6) == g["dense_fp64_MB"]
+    assert 1 - A.nnz / (A.shape[0] * A.shape[1]) >= g["zero_fraction_at_least"]
+
+
+def test_paper_counts_3d():
+    """P:245 '32x32x32 (220k variables and 420k constraints) ... 780GB and for 64x64x64
+    we would need 50k GB'; P:249 '99.999% zeros for a 64x64x64 matrix'."""
+    g = json.load(open(os.path.join(GOLD, "paper_counts.json")))
+    pr = Problem((32, 32, 32), (0.1, 0.1, 0.1))
+    rng = np.random.default_rng(1)
+    A, _, _ = assemble(pr, _rand_c((32, 32, 32), rng), np.zeros(pr.P), np.zeros(pr.P))
+    n_c, n_v = A.shape
+    assert (n_v, n_c) == counts((32, 32, 32))
+    gg = g["32x32x32"]
+    assert int(n_v / 1e4) * 1e4 == pytest.approx(gg["n_v_approx"], rel=0.05)  # "220k"
+    assert int(n_c / 1e4) * 1e4 == pytest.approx(gg["n_c_approx"], rel=0.02)  # "420k"
+    assert int(n_c * n_v * 8 / 1e9 / 10) * 10 == gg["dense_fp64_GB_approx"]     # "780GB"
+    n_v3, n_c3 = counts((64, 64, 64))
+    assert round(n_v3 * n_c3 * 8 / 1e9 / 1e3) * 1e3 == g["64x64x64"]["dense_fp64_GB_approx"]
+    # sparsity at 64^3: the row nnz per group is fixed by Eqs. 3-7 and measured at 32^3
+    nnz_per_point = A.nnz / pr.P
+    assert 1 - nnz_per_point * 64 ** 3 / (n_v3 * n_c3) >= g["64x64x64"]["zero_fraction_at_least"]
+
+
+def test_row_groups_counted_separately():
+    """n_c = P + |B| + 2D P + sum_d 2(n_d-1)P/n_d with B = all faces (reading Q1); the
+    t=0-only boundary of SPEC.md would give 9182 at 32x32, not the printed 9212."""
+    shape = (32, 32)
+    nb_all = int(boundary_mask(shape).sum())
+    assert nb_all == 124
+    nb_t0_only = 32 + 2 * 31
+    assert 1024 + nb_t0_only + 4096 + 3968 == 9182 != 9212
+
+
+# ----------------------------------------------------------- stencils / MMS (P2, P3)
+@pytest.mark.parametrize("n", [6, 7, 11])
+@pytest.mark.parametrize("k", [1, 2])
+def test_fd_stencils_exact_on_quartics(n, k):
+    """5-point stencils are exact on polynomials of degree <= 4 at every index,
+    including the one-sided edge stencils (reading Q4)."""
+    rng = np.random.default_rng(n * 10 + k)
+    coef = rng.normal(size=5)
+    x = np.arange(n, dtype=np.float64)
+    f = np.polyval(coef, x)
+    df = np.polyval(np.polyder(coef, k), x)
+    for i in range(n):
+        offs, w = fd_stencil(k, i, n)
+        assert np.all((i + offs >= 0) & (i + offs < n))
+        assert np.dot(w, f[i + offs]) == pytest.approx(df[i], rel=1e-10, abs=1e-8)
+
+
+def test_eq5_three_point_reading():
+    """Eq. 5 with a 3-point stencil reads s^2 u_m = u_prev - 2u + u_next; our
+    central 5-point a^2 reduces to the same second difference on quadratics."""
+    offs, w = fd_stencil(2, 5, 12)
+    x = np.arange(12.0)
+    f = 3 * x ** 2 - x + 2
+    assert np.dot(w, f[5 + offs]) == pytest.approx(f[4] - 2 * f[5] + f[6])
+
+
+@pytest.mark.parametrize("shape,h", [((8, 9), (0.1, 0.2)), ((6, 7, 8), (0.05, 0.1, 0.15)),
+                                     ((16, 16), (1 / 15, 1 / 15))])
+def test_mms_rows_exact(shape, h):
+    """P2: a per-dim-quadratic u with b := sum c_m d_m u (Eq. 1) and omega := u makes
+    every row of Eqs. 3-7 hold exactly, for any weights."""
+    rng = np.random.default_rng(3)
+    D = len(shape)
+    X = _coords(shape, h)
+    alpha = rng.normal(size=(3,) * D)
+    # u = sum alpha_e prod x_d^e_d and its pure derivatives
+    def basis(e, d, kk):
+        v = X[d] ** e if kk == 0 else (e * X[d] ** max(e - 1, 0) if kk == 1 else
+                                      e * (e - 1) * X[d] ** max(e - 2, 0))
+        return v
+    fields = []
+    for which in [None] + [(d, k) for d in range(D) for k in (1, 2)]:
+        out = np.zeros(shape)
+        for e in np.ndindex(*(3,) * D):
+            term = alpha[e] * np.ones(shape)
+            for d in range(D):
+                term = term * basis(e[d], d, 0 if which is None or which[0] != d else which[1])
+            out += term
+        fields.append(out.reshape(-1))
+    z = np.concatenate(fields)
+    c = _rand_c(shape, rng)
+    b = (c * z.reshape(1 + 2 * D, -1)).sum(0)
+    pr = Problem(shape, h, w_eq=1.3, w_bnd=2.0, w_der=0.7, w_sm=0.9)
+    A, d, _ = assemble(pr, c, b, fields[0])
+    assert np.abs(A @ z - d).max() <= 1e-11 * max(1.0, np.abs(d).max())
+    if pr.n_v <= 5000:
+        f = solve_forward(pr, c, b, fields[0])
+        assert np.linalg.norm(f["z"] - z) <= 1e-9 * np.linalg.norm(z)
+
+
+def test_constants_satisfy_derivative_and_smoothness_rows():
+    """P3: u == const, all derivative variables 0, satisfies Eqs. 5-7 exactly."""
+    shape, h = (7, 9, 6), (0.3, 0.2, 0.1)
+    pr = Problem(shape, h)
+    rng = np.random.default_rng(4)
+    A, _, info = assemble(pr, _rand_c(shape, rng), np.zeros(pr.P), np.zeros(pr.P))
+    z = np.zeros(pr.n_v)
+    z[:pr.P] = 2.5
+    r = A @ z
+    first_der_row = pr.P + info["bnd_points"].size
+    assert np.abs(r[first_der_row:]).max() < 1e-12
+
+
+# ------------------------------------------------------------------ P4 bubble
+def _bubble(shape, h):
+    X = _coords(shape, h)
+    D = len(shape)
+    L = [(n - 1) * hh for n, hh in zip(shape, h)]
+    fac = [X[d] * (L[d] - X[d]) for d in range(D)]
+    beta = np.prod(fac, axis=0)
+    fields = [beta]
+    for d in range(D):
+        rest = np.prod([fac[j] for j in range(D) if j != d], axis=0) if D > 1 else 1.0
+        fields.append((L[d] - 2 * X[d]) * rest)
+        fields.append(-2.0 * rest * np.ones(shape))
+    return np.stack([f.reshape(-1) for f in fields])
+
+
+@pytest.mark.parametrize("shape,h", [((8, 9), (0.1, 0.2)), ((6, 7, 8), (0.2, 0.1, 0.3))])
+def test_bubble_null_vector(shape, h):
+    """P4: beta = prod x_d (L_d - x_d) vanishes on all faces and is quadratic per dim, so
+    with c == 0 it satisfies every boundary/derivative/smoothness row: A z_bub = 0, and
+    it is the only null vector (second-smallest singular value is O(1e-3))."""
+    pr = Problem(shape, h)
+    zb = _bubble(shape, h).reshape(-1)
+    A, _, _ = assemble(pr, np.zeros((pr.M, pr.P)), np.zeros(pr.P), np.zeros(pr.P))
+    assert np.linalg.norm(A @ zb) <= 1e-13 * np.linalg.norm(zb) * np.abs(A).max()
+    s = np.linalg.svd(A.toarray(), compute_uv=False)
+    assert s[-1] < 1e-12 * s[0]
+    assert s[-2] > 1e-5 * s[0]
+
+
+def test_bubble_quadratic_form_general_c():
+    """P4 for general c: <z_bub, A^T A z_bub> = w_eq^2 sum_p (sum_m c_m d_m beta)^2
+    because only the equation rows (Eq. 3) see the bubble."""
+    shape, h = (7, 8, 9), (0.1, 0.15, 0.2)
+    rng = np.random.default_rng(5)
+    pr = Problem(shape, h, w_eq=1.7, w_bnd=0.6, w_der=2.0, w_sm=0.8)
+    c = _rand_c(shape, rng)
+    zb = _bubble(shape, h)
+    A, _, _ = assemble(pr, c, np.zeros(pr.P), np.zeros(pr.P))
+    lhs = zb.reshape(-1) @ normal_apply(A, zb.reshape(-1))
+    rhs = pr.w_eq ** 2 * ((c * zb).sum(0) ** 2).sum()
+    assert lhs == pytest.approx(rhs, rel=1e-11)
+
+
+# ---------------------------------------------------------- P5/P6 KKT + hand cases
+def test_hand_cases():
+    """P6: closed-form least squares (tests/golden/hand_cases.json)."""
+    g = json.load(open(os.path.join(GOLD, "hand_cases.json")))
+    for key in ("one_by_one", "two_by_one"):
+        case = g[key]
+        A = sp.csr_matrix(np.array(case["A"]))
+        z, lam = lstsq_forward(A, np.array(case["d"]), method="dense")
+        assert np.allclose(z, case["z"], atol=1e-12)
+        assert np.allclose(lam, case["lam"], atol=1e-12)
+        dz, dlam, dA, dd = lstsq_backward(A, z, lam, np.array(case["g"]), method="dense")
+        assert np.allclose(dA.toarray(), case["dA"], atol=1e-12)
+        assert np.allclose(dd, case["dd"], atol=1e-12)
+        assert np.allclose(dlam + A @ dz, 0.0)          # Eq. 11 first block row
+        assert np.allclose(A.T @ dlam, -np.array(case["g"]))  # Eq. 11 second block row
+
+
+@pytest.mark.parametrize("method", ["dense", "lu", "cg"])
+def test_kkt_identities(method):
+    """P5: A^T lambda* = 0 (Eq. 10 second block row, LS optimality) and lambda* = d - A z*."""
+    cfg = synth.CONFIGS["C1"]
+    bt = synth.make_batch("C1")
+    pr = Problem(cfg.shape, cfg.h)
+    f = solve_forward(pr, bt["c"][0], bt["b"][0], bt["omega"][0], method=method)
+    A, d = f["A"], f["d"]
+    assert np.linalg.norm(A.T @ f["lam"]) <= 1e-10 * np.linalg.norm(A.T @ d)
+    assert np.allclose(f["lam"], d - A @ f["z"])
+
+
+@pytest.mark.parametrize("shape,h", [((16, 16), (1 / 15, 1 / 15)), ((8, 8, 8), (0.1, 0.1, 0.1))])
+def test_solver_crosscheck(shape, h):
+    """P9: SVD-lstsq, equilibrated SuperLU + refinement and Jacobi-CG agree to 1e-9."""
+    rng = np.random.default_rng(6)
+    pr = Problem(shape, h)
+    c = _rand_c(shape, rng)
+    b = rng.normal(size=pr.P)
+    om = rng.normal(size=pr.P)
+    zs = [solve_forward(pr, c, b, om, method=m)["z"] for m in ("dense", "lu", "cg")]
+    for z in zs[1:]:
+        assert np.linalg.norm(z - zs[0]) <= 1e-9 * np.linalg.norm(zs[0])
+
+
+# ---------------------------------------------------------- P7 finite differences
+def test_field_gradients_match_central_differences():
+    """P7: grad_c, grad_b, grad_omega of l = <g, z*> (P:240 chained through Eqs. 3-4)
+    match central finite differences of the forward solve; grad_omega = 0 off B."""
+    shape, h = (8, 9), (0.1, 0.2)
+    rng = np.random.default_rng(7)
+    pr = Problem(shape, h, w_eq=1.3, w_bnd=2.0, w_der=0.7, w_sm=0.9)
+    c = _rand_c(shape, rng)
+    b = rng.normal(size=pr.P)
+    om = rng.normal(size=pr.P)
+    g = rng.normal(size=pr.n_v)
+    f = solve_forward(pr, c, b, om, method="dense")
+    bw = solve_backward(pr, f, g, method="dense")
+
+    def loss(c_, b_, om_):
+        return g @ solve_forward(pr, c_, b_, om_, method="dense")["z"]
+
+    eps = 1e-6
+    scale = max(np.abs(bw["grad_c"]).max(), np.abs(bw["grad_b"]).max())
+    bmask = boundary_mask(shape)
+    for _ in range(6):
+        m, p = rng.integers(pr.M), rng.integers(pr.P)
+        cp, cm = c.copy(), c.copy()
+        cp[m, p] += eps
+        cm[m, p] -= eps
+        fd = (loss(cp, b, om) - loss(cm, b, om)) / (2 * eps)
+        assert abs(fd - bw["grad_c"][m, p]) <= 1e-6 * scale
+        p = rng.integers(pr.P)
+        bp, bm = b.copy(), b.copy()
+        bp[p] += eps
+        bm[p] -= eps
+        fd = (loss(c, bp, om) - loss(c, bm, om)) / (2 * eps)
+        assert abs(fd - bw["grad_b"][p]) <= 1e-6 * scale
+    for p in list(np.flatnonzero(bmask)[:4]) + list(np.flatnonzero(~bmask)[:2]):
+        op, omm = om.copy(), om.copy()
+        op[p] += eps
+        omm[p] -= eps
+        fd = (loss(c, b, op) - loss(c, b, omm)) / (2 * eps)
+        assert abs(fd - bw["grad_omega"][p]) <= 1e-6 * scale
+        if not bmask[p]:
+            assert bw["grad_omega"][p] == 0.0
+
+
+def test_pointwise_gradient_forms():
+    """a10: the outer-product form of P:240 restricted to c, b, omega equals the
+    pointwise forms w_eq^2 (rho dz - gamma z), w_eq^2 gamma, w_bnd^2 dz_phi on B."""
+    shape, h = (8, 9), (0.1, 0.2)
+    rng = np.random.default_rng(8)
+    pr = Problem(shape, h, w_eq=1.3, w_bnd=2.0, w_der=0.7, w_sm=0.9)
+    c = _rand_c(shape, rng)
+    b = rng.normal(size=pr.P)
+    om = rng.normal(size=pr.P)
+    g = rng.normal(size=pr.n_v)
+    f = solve_forward(pr, c, b, om, method="dense")
+    bw = solve_backward(pr, f, g, method="dense")
+    z = f["z"].reshape(pr.M, -1)
+    dz = bw["dz"].reshape(pr.M, -1)
+    rho = b - (c * z).sum(0)
+    gam = (c * dz).sum(0)
+    assert np.allclose(bw["grad_c"], pr.w_eq ** 2 * (rho * dz - gam * z), atol=1e-12)
+    assert np.allclose(bw["grad_b"], pr.w_eq ** 2 * gam, atol=1e-12)
+    assert np.allclose(bw["grad_omega"], pr.w_bnd ** 2 * dz[0] * boundary_mask(shape), atol=1e-12)
+
+
+# ------------------------------------------------------------ P8 analytic solutions
+def _analytic(kind, n, w_der):
+    h = 1 / (n - 1)
+    T, X = _coords((n, n), (h, h))
+    c = np.zeros((5, n, n))
+    if kind == "heat":      # u_t = 0.1 u_xx, u = exp(-0.1 pi^2 t) sin(pi x)  (Table 1)
+        c[1], c[4] = 1.0, -0.1
+        ex = np.exp(-0.1 * np.pi ** 2 * T) * np.sin(np.pi * X)
+    else:                   # Laplace, u = sin(pi x) sinh(pi t)/sinh(pi)  (§6.1)
+        c[2], c[4] = 1.0, 1.0
+        ex = np.sin(np.pi * X) * np.sinh(np.pi * T) / np.sinh(np.pi)
+    pr = Problem((n, n), (h, h), w_der=w_der)
+    f = solve_forward(pr, c.reshape(5, -1), np.zeros(n * n), ex.reshape(-1),
+                      method="dense" if n <= 16 else "lu")
+    u = f["z"][:n * n]
+    return np.linalg.norm(u - ex.reshape(-1)) / np.linalg.norm(ex)
+
+
+@pytest.mark.parametrize("kind", ["heat", "laplace"])
+@pytest.mark.parametrize("w_der", [1.0, 12.0])
+def test_analytic_convergence(kind, w_der):
+    """P8: the converged LS solution approaches the analytic solution as h -> 0 (within
+    discretisation error; the paper's 1e-1..1e-2 vs py-pde P:468 are looser bounds).
+    Literal Eq. 5 (w_der = 1) converges at >= 2nd order, the 12h^k scaling at >= 4th."""
+    e16, e32 = _analytic(kind, 16, w_der), _analytic(kind, 32, w_der)
+    assert e16 < 1e-3
+    assert e16 / e32 > (4.0 if w_der == 1.0 else 16.0)
+    assert e32 < 1e-1 * 1e-2  # far inside the paper's 32x32 error of order 1e-1
+
+
+# ------------------------------------------------------------ synth sanity
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_synth_mms_consistent_at_config_sizes(name):
+    """P2 at every config size: the MMS twin's closed-form z* satisfies A z* = d up to
+    the float32 rounding of b and omega (relative normal residual <= 1e-6)."""
+    m = synth.make_mms(name, batch=1)
+    cfg = m["cfg"]
+    pr = Problem(cfg.shape, cfg.h)
+    A, d, _ = assemble(pr, m["c"][0], m["b"][0], m["omega"][0])
+    z = m["z_exact"][0].reshape(-1)
+    r = A.T @ (d - A @ z)
+    assert np.linalg.norm(r) <= 1e-6 * np.linalg.norm(A.T @ d)
+
+
+def test_synth_deterministic_float32():
+    a = synth.make_batch("C4", batch=2)
+    b = synth.make_batch("C4", batch=2)
+    assert a["c"].dtype == np.float32 and a["c"].shape == (2, 7, 32 * 64 * 64)
+    assert np.array_equal(a["c"], b["c"]) and np.array_equal(a["omega"], b["omega"])
+    assert not np.array_equal(a["c"][0], a["c"][1])
+    assert field_index(2, 2) == 6
