@@ -1,0 +1,212 @@
+/*
+ * mpde.h -- C ABI of the B200-native NeuRLP-PDE batched solver
+ * (Mechanistic PDE Networks, arXiv 2502.18377, §3).
+ *
+ * The library solves, for a batch of B independent linear space-time PDEs
+ *      sum_m c_m(p) u_m(p) = b(p)           (Eq. 1)
+ * the least-squares problem min_z ||A z - d||_2 whose rows are the equation
+ * (Eq. 3), Dirichlet boundary (Eq. 4), derivative (Eq. 5,
+ * P:169-174) and forward/backward Taylor smoothness (Eqs. 6-7)
+ * constraints, via the normal equations A^T A z = A^T d (Eq. 9), and the
+ * backward pass A^T A d_z = g_z (Eq. 11) with the gradient formulas of
+ * P:240 restricted to the encoder outputs c, b, omega.
+ *
+ * Readings of the paper that fix the operator: the boundary
+ * set B is every face of the space-time box; the variables are u_phi plus the first
+ * and second pure derivative along every dim (|M| = 1 + 2*ndim, field order
+ * phi, d0, d00, d1, d11, ...); derivative rows use 5-point central weights for
+ * 2 <= i <= n-3 and one-sided 5-point weights at the two points nearest each edge,
+ * with coefficient h^k on the derivative variable (literal Eq. 5); Taylor rows are
+ * present in each direction where the neighbour exists.
+ *
+ * Layout: every per-point tensor is C-contiguous float32 with dim 0 (time) slowest:
+ *   coeff  [B][|M|][n0][n1]...      c_m, field-major per PDE
+ *   rhs_b  [B][n0][n1]...           b
+ *   bnd    [B][n0][n1]...           omega (only entries on B are read)
+ *   z, g_z, dz, grad_coeff  [B][|M|][P]
+ *   grad_rhs, grad_bnd      [B][P]
+ * All tensor pointers passed to mpde_build_hierarchy / mpde_solve_* /
+ * mpde_apply_* are DEVICE pointers owned by the caller (PyTorch allocates); the
+ * library performs no device allocation in those calls -- all scratch lives in the
+ * caller's workspace (size from mpde_workspace_bytes).  Calls enqueue work on
+ * `stream` and, unless stated otherwise, return without synchronising.  A handle
+ * must not be used from two host threads at once.
+ *
+ * Errors: every int-returning call returns an MPDE_* code; synchronous failures
+ * (bad arguments, unsupported configuration, workspace too small, CUDA launch
+ * failure) return non-zero and set a thread-local message (mpde_last_error()).
+ * Per-PDE numerical outcomes (not converged, non-finite input, indefinite
+ * operator) are asynchronous and reported in mpde_stats.status.
+ */
+#ifndef MPDE_H_
+#define MPDE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* mpde_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+enum {
+  MPDE_OK = 0,
+  MPDE_ERR_INVALID_ARG = 1,   /* null pointer, batch < 1, non-finite step, ...        */
+  MPDE_ERR_SHAPE = 2,         /* ndim not in {2,3}, a dim with fewer than 6 points    */
+  MPDE_ERR_UNSUPPORTED = 3,   /* deriv_order != 2, unknown smoother/coarse option     */
+  MPDE_ERR_NONFINITE = 4,     /* (status only) non-finite input or residual           */
+  MPDE_ERR_NOT_CONVERGED = 5, /* (status only) tolerance not met within the limits    */
+  MPDE_ERR_CUDA = 6,          /* a CUDA call failed; message has the CUDA error text  */
+  MPDE_ERR_WORKSPACE = 7      /* workspace_bytes smaller than mpde_workspace_bytes()  */
+};
+
+/* per-PDE status values in mpde_stats.status */
+enum { MPDE_STATUS_CONVERGED = 0, MPDE_STATUS_MAXITER = 1, MPDE_STATUS_NONFINITE = 2,
+       MPDE_STATUS_INDEFINITE = 3 };
+
+/* Grid, batch and row-group weights.  P:89 (Cartesian grid), P:111-117 (uniform step
+ * per dim -- learned per-interval steps are out of scope), P:147-151 (variables). */
+typedef struct {
+  int32_t ndim;        /* grid dims including time: 2 or 3; dim 0 = time (slowest)      */
+  int32_t n[4];        /* points per dim, each >= 6 (5-point one-sided edge stencils)   */
+  double  h[4];        /* uniform step per dim, finite, > 0                             */
+  int32_t batch;       /* B >= 1 independent PDEs                                        */
+  int32_t deriv_order; /* must be 2: M = {phi, d_k, d_kk for every dim}                 */
+  float   w_eq, w_bnd, w_deriv, w_smooth; /* row-group weights, > 0 (paper: all 1)      */
+} mpde_problem;
+
+/* Solver options.  The Krylov method is PCG on the (condensed) normal equations; the
+ * preconditioner is one multigrid V-cycle (Alg. 1). */
+typedef struct {
+  float   tol;        /* stop when ||A^T(d - A z)|| / ||A^T d|| <= tol (fp64 residual)   */
+  float   tol_inner;  /* PCG stop per refinement pass: ||r_k|| / ||r_0|| <= tol_inner    */
+  int32_t max_iters;  /* PCG iteration cap per refinement pass                          */
+  int32_t max_refine; /* fp64-residual refinement passes (>= 1)                          */
+  int32_t smoother;   /* 0 = damped Jacobi, 1 = Chebyshev-accelerated Jacobi             */
+  int32_t nu;         /* smoothing steps, pre = post (>= 1)                              */
+  int32_t coarsest;   /* stop coarsening a dim once it is <= coarsest (8)         */
+  int32_t levels_max; /* cap on the number of levels (1 = no multigrid: Jacobi-PCG)      */
+  int32_t poll_every; /* host convergence poll interval in PCG iterations (>= 1)         */
+  float   jacobi_theta;   /* damped Jacobi: omega = theta / lambda_max(D^-1 S)           */
+  float   cheb_ratio;     /* Chebyshev interval [lambda_max/ratio, 1.1 lambda_max]       */
+  int32_t lanczos_steps;  /* Lanczos steps (2..32) estimating lambda_max per level+PDE  */
+  int32_t precision;  /* arithmetic (storage is fp32): 0 = fp32 everywhere; 1 = fp64 for
+                         the condensation and the PCG operator (default); 2 = fp64 in the
+                         V-cycle too.  The refinement residual is always fp64.          */
+} mpde_options;
+
+/* one per PDE, device memory, written by mpde_solve_fwd / mpde_solve_bwd */
+typedef struct {
+  int32_t iters;    /* PCG iterations summed over refinement passes                       */
+  int32_t refines;  /* refinement passes run                                              */
+  int32_t status;   /* MPDE_STATUS_*                                                      */
+  float   rel_res;  /* final ||A^T(d - A z)|| / ||A^T d|| (fp64 residual)                 */
+} mpde_stats;
+
+typedef struct mpde_hierarchy mpde_hierarchy; /* opaque, host-side handle */
+
+/* Defaults: tol 1e-7, tol_inner 1e-4, max_refine 6, Chebyshev nu = 2, coarsest 8,
+ * 16 Lanczos steps, precision 1. */
+mpde_options mpde_default_options(void);
+
+/* n_v = |M| * P variables, n_c constraint rows (Eqs. 3-7 counted), levels of the
+ * hierarchy for these options.  Any output pointer may be NULL. */
+int mpde_sizes(const mpde_problem* prob, const mpde_options* opts, int64_t* n_v,
+               int64_t* n_c, int32_t* n_levels);
+
+/* Bytes of device workspace mpde_build_hierarchy needs (0 on invalid input). */
+size_t mpde_workspace_bytes(const mpde_problem* prob, const mpde_options* opts);
+
+/* Build the multigrid hierarchy for coefficient fields `coeff` [B][|M|][P] (device):
+ * coarse coefficient fields by full-weighting averaging, the diagonal of each
+ * level's condensed operator, per-PDE lambda_max estimates and the coarsest-level
+ * inverse.  `coeff` and `workspace` must stay valid and unmodified until
+ * mpde_destroy_hierarchy.  Asynchronous on `stream`.  *out receives a new handle. */
+int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts,
+                         const float* coeff, void* workspace, size_t workspace_bytes,
+                         mpde_stream_t stream, mpde_hierarchy** out);
+
+/* Forward pass: z* = argmin ||A z - d|| for every PDE of the batch.
+ * rhs_b [B][P], bnd [B][P] (device, read);  z [B][|M|][P] (device, written);
+ * stats: device array of B mpde_stats or NULL.  Synchronises `stream` only to poll
+ * convergence every poll_every iterations. */
+int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, float* z,
+                   mpde_stats* stats, mpde_stream_t stream);
+
+/* Backward pass (Eq. 11) for the loss gradient g_z = dl/dz* [B][|M|][P]:
+ * solves A^T A d_z = g_z with the same hierarchy and writes
+ *   grad_coeff[b][m][p] = dl/dc_m(p),  grad_rhs[b][p] = dl/db(p),
+ *   grad_bnd[b][p] = dl/domega(p) (0 off the boundary set),  dz_opt = d_z (or NULL).
+ * z must be the forward solution for the same rhs_b.  If the last mpde_solve_fwd on this
+ * handle was called with the same rhs_b pointer, the equation residual b - c.z* it kept
+ * (formed from its fp64 solution) is used for grad_coeff; otherwise it is formed from the
+ * fp32 z, which loses accuracy where the derivative fields are large. */
+int mpde_solve_bwd(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,
+                   float* grad_coeff, float* grad_rhs, float* grad_bnd, float* dz_opt,
+                   mpde_stats* stats, mpde_stream_t stream);
+
+/* Release the handle (does not free caller memory). */
+int mpde_destroy_hierarchy(mpde_hierarchy* h);
+
+/* Thread-local text of the last synchronous error ("" if none). */
+const char* mpde_last_error(void);
+
+/* ---- operator-level entry points (used by the parity tests) ------------------- */
+
+/* q = A^T A z for the fine level of `prob` (Eq. 9), fp64 accumulation, device
+ * pointers coeff [B][|M|][P], z [B][|M|][P], q [B][|M|][P]. */
+int mpde_apply_normal(const mpde_problem* prob, const float* coeff, const float* z, float* q,
+                      mpde_stream_t stream);
+
+/* y = S_l x on level `level` of a built hierarchy, where S_l is the Schur complement of
+ * the level's normal matrix onto the u_phi variables.
+ * x, y: device [B][P_l]. */
+int mpde_apply_schur(mpde_hierarchy* h, int32_t level, const float* x, float* y,
+                     mpde_stream_t stream);
+
+/* z = M^-1 r: one V-cycle of the preconditioner (Alg. 1) on the fine level,
+ * r, z: device [B][P].  The preconditioner is a fixed symmetric linear map. */
+int mpde_apply_precond(mpde_hierarchy* h, const float* r, float* z, mpde_stream_t stream);
+
+/* Copy internal per-level data to the caller (device pointer `dst`):
+ *   what = 0: level shape (n0, n1, n2, levels) -> dst is HOST int32[4] (synchronous)
+ *   what = 1: 1/diag(S_l) [B][P_l] fp32        what = 2: lambda_max [B] fp32
+ *   what = 3: coarse coefficients [B][|M|][P_l] fp32
+ *   what = 4: coarsest-level inverse [B][P_c][P_c] fp32 (level ignored) */
+int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* dst,
+                         mpde_stream_t stream);
+
+/* Host-buffer end-to-end call: copies the inputs from HOST memory (pinned for
+ * asynchrony) into `device_staging` (>= mpde_host_staging_bytes), builds the
+ * hierarchy in `workspace`, runs forward + backward with g_z, and copies z, grad_coeff,
+ * grad_rhs, grad_bnd back to HOST memory.  Synchronises `stream` before returning. */
+size_t mpde_host_staging_bytes(const mpde_problem* prob);
+int mpde_fwd_bwd_host(const mpde_problem* prob, const mpde_options* opts,
+                      const float* coeff_h, const float* rhs_h, const float* bnd_h,
+                      const float* gz_h, float* z_h, float* grad_coeff_h, float* grad_rhs_h,
+                      float* grad_bnd_h, void* device_staging, void* workspace,
+                      size_t workspace_bytes, mpde_stream_t stream);
+
+/* out[j] = sum_b x[b][j] for x [batch][n] (device, fixed summation order): the
+ * batch-summed coefficient gradient that the multi-GPU step all-reduces (NCCL). */
+int mpde_batch_sum(const float* x, int32_t batch, int64_t n, float* out, mpde_stream_t stream);
+
+/* ---- launch profiler (process-wide, not thread-safe; off by default) ------------
+ * Between begin and end every library launch is bracketed by CUDA events on the
+ * stream it is launched on.  end() synchronises and returns, per launch class,
+ * the summed event time (ms) and the launch count; pts[0..7] = points processed by the
+ * S pass-2 kernel per epilogue kind, pts[8] = points processed by the S pass-1 kernel.
+ * Classes: 0 S pass 1 (schur_g), 1 S pass 2 (schur_out), 2 fp64 residual, 3 condense,
+ * 4 back-substitution, 5 grid transfers, 6 PCG/smoother vector ops, 7 per-PDE scalar
+ * logic, 8 coarsest solve, 9 hierarchy build, 10 forward/backward epilogues. */
+#define MPDE_PROF_NCLASS 11
+/* Number of kernel launches this process has issued through the library so far. */
+uint64_t mpde_launch_count(void);
+int mpde_profile_begin(void);
+int mpde_profile_end(double* ms, int64_t* launches, uint64_t* pts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPDE_H_ */

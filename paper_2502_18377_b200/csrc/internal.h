@@ -1,0 +1,132 @@
+// internal.h -- host-visible declarations shared by kernels.cu and mpde.cu
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mpde.h"
+#include "common.cuh"
+
+namespace mpde {
+
+enum {
+  EPI_STORE = 0,
+  EPI_DOT = 1,
+  EPI_POWER = 2,
+  EPI_RESID = 3,
+  EPI_SMOOTH = 4,
+  EPI_SMOOTH_LAST = 5,
+  EPI_POST0 = 6
+};
+
+enum {
+  SC_RHSNORM = 0,
+  SC_REFRES = 1,
+  SC_PASS_BEGIN = 2,
+  SC_INIT = 3,
+  SC_RZ0 = 4,
+  SC_ALPHA = 5,
+  SC_CONV = 6,
+  SC_BETA = 7,
+  SC_LZ_RESET = 8,
+  SC_REACT = 9,
+  SC_LZ_ALPHA = 10,
+  SC_LZ_BETA = 11,
+  SC_LZ_EIG = 12
+};
+
+struct EpiArgs {
+  float* y = nullptr;        // STORE / DOT / POWER output
+  float* res = nullptr;      // smoother residual (in/out)
+  float* d_out = nullptr;    // next smoother direction
+  float* e = nullptr;        // smoother error accumulator
+  const float* dinv = nullptr;
+  const float* coef = nullptr;  // per PDE [2*nu] (alpha_k, beta_k)
+  int coef_stride = 0;
+  int step = 0;
+  const float* rdot = nullptr;  // optional dot partner
+  double* part = nullptr;       // per (vector, tile) partial sums
+  unsigned long long* pts = nullptr;  // profiling: points processed per EPI (or nullptr)
+};
+
+// per-PDE device state (arrays of length B)
+struct PdeState {
+  double* rz;
+  double* rr0;
+  double* rhsn;
+  double* relres;
+  double* lmax;
+  double* lz;      // [B][64] Lanczos tridiagonal (alpha[0..31], beta[32..63])
+  float* alpha;
+  float* beta;
+  int* act;
+  int* done;
+  int* iters;
+  int* pass_iters;
+  int* refines;
+  int* status;
+  int* inpass;
+  int* failed;
+  float tol;
+};
+
+int ntiles(int P);
+extern unsigned long long g_launch_count;  // host-side count of kernel launches
+int coarse_gemv_blocks(int n);
+void upload_constants();
+
+void launch_rhs_init(const Geo& G, int B, const float* c, const float* b, const float* om,
+                     float* rhs, double* part, cudaStream_t s);
+void launch_residual64(const Geo& G, int B, const float* c, const float* rhs, const float* b,
+                       const float* om, const double* z64, float* r, double* part, const int* act,
+                       cudaStream_t s);
+void launch_apply_normal(const Geo& G, int B, const float* c, const float* z, float* q,
+                         cudaStream_t s);
+void launch_ndd_solve(const Geo& G, int B, const float* c, const float* r, float* t,
+                      const int* act, bool f64, cudaStream_t s);
+void launch_schur_rhs(const Geo& G, int B, const float* c, const float* r, const float* t,
+                      float* rt, const int* act, bool f64, cudaStream_t s);
+void launch_backsub(const Geo& G, int B, const float* c, const float* r, const float* dphi,
+                    double* z64, const int* act, bool f64, cudaStream_t s);
+// g: per-point scratch, float or double (f64) -- allocate 8 bytes per point
+void launch_schur_g(const Geo& G, int nvec, int crep, const float* c, const float* x, void* g,
+                    const int* act, unsigned long long* pts, bool f64, cudaStream_t s);
+void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* c, const float* x,
+                      const void* g, const EpiArgs& A, const int* act, bool f64, cudaStream_t s);
+void launch_diag_schur(const Geo& G, int B, const float* c, float* dinv, cudaStream_t s);
+void launch_restrict(const Geo& Gf, const Geo& Gc, int nvec, int nfield, const float* fine,
+                     float* coarse, const int* act, int crep, cudaStream_t s);
+void launch_prolong(const Geo& Gf, const Geo& Gc, int nvec, const float* coarse, float* fine,
+                    const int* act, cudaStream_t s);
+void launch_smooth_start(int P, int nvec, const float* r, const float* dinv, const float* coef,
+                         int coef_stride, float* res, float* d, float* e, const int* act,
+                         cudaStream_t s);
+void launch_pcg_update(int P, int nvec, const float* alpha, const float* p, const float* q,
+                       float* x, float* r, double* part, const int* act, cudaStream_t s);
+void launch_p_update(int P, int nvec, const float* beta, const float* z, float* p,
+                     const int* act, cudaStream_t s);
+void launch_scale(int P, int nvec, const float* sc, const float* x, float* y, const int* act,
+                  cudaStream_t s);
+void launch_lz_update(int P, int nvec, const float* y, const float* v, float* vprev,
+                      const float* dinv, const float* alpha, const float* beta, double* part,
+                      cudaStream_t s);
+void launch_rand_fill(int P, int nvec, float* y, uint32_t seed, cudaStream_t s);
+void launch_identity(int Pc, int nvec, float* x, cudaStream_t s);
+void launch_coarse_invert(int n, int B, const float* cols, double* scratch, float* inv,
+                          cudaStream_t s);
+void launch_coarse_gemv(int n, int nvec, const float* sinv, const float* r, float* e,
+                        const float* rdot, double* part, const int* act, cudaStream_t s);
+void launch_scalar(int op, int B, const PdeState& st, const double* part, int nt, float tol2,
+                   int max_iters, cudaStream_t s);
+void launch_count_active(int B, const int* act, int* out, cudaStream_t s);
+void launch_smooth_coef(int B, int nu, int kind, float theta, float ratio, const double* lmax,
+                        float* coef, cudaStream_t s);
+void launch_grad(const Geo& G, int B, const float* c, const float* b, const float* z,
+                 const float* rho, const double* dz64, float* gc, float* gb, float* gw,
+                 float* dz_out, cudaStream_t s);
+void launch_fwd_out(const Geo& G, int B, const float* c, const float* b, const double* z64,
+                    float* z, float* rho, cudaStream_t s);
+void launch_d2f(size_t n, const double* a, float* b, cudaStream_t s);
+void launch_batch_sum(const float* x, int B, int64_t n, float* out, cudaStream_t s);
+void launch_stats_out(int B, const PdeState& st, mpde_stats* out, cudaStream_t s);
+
+}  // namespace mpde

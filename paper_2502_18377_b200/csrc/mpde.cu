@@ -1,0 +1,839 @@
+// mpde.cu -- host side of the C ABI (include/mpde.h): validation, workspace planning,
+// hierarchy build and the refinement / PCG / V-cycle orchestration.
+//
+// Forward and backward (Eq. 11) share one solve core:
+//   z64 = 0
+//   repeat (max_refine passes, fp64 residual):
+//     r   = rhs - N z64                      (fp64 accumulation, K9)
+//     t   = N_dd^-1 r_d ; rt = r_phi - (N (0,t))_phi      (condense)
+//     PCG on S dphi = rt, preconditioned by one V-cycle    (Alg. 1)
+//     z64 += (dphi, N_dd^-1 (r_d - (N (dphi,0))_d))         (back-substitute)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace mpde;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return set_err(MPDE_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKL()                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = cudaGetLastError();                                              \
+    if (e_ != cudaSuccess)                                                            \
+      return set_err(MPDE_ERR_CUDA, "kernel launch failed (%s:%d): %s", __FILE__, __LINE__, \
+                     cudaGetErrorString(e_));                                         \
+  } while (0)
+
+constexpr int kMaxLevels = 10;
+
+struct LevelShape {
+  int n[kMaxD];
+  int P;
+};
+
+int validate(const mpde_problem* pr, const mpde_options* op) {
+  if (!pr || !op) return set_err(MPDE_ERR_INVALID_ARG, "null problem/options");
+  if (pr->ndim < 2 || pr->ndim > 3)
+    return set_err(MPDE_ERR_SHAPE, "ndim must be 2 or 3 (got %d)", pr->ndim);
+  if (pr->deriv_order != 2)
+    return set_err(MPDE_ERR_UNSUPPORTED, "deriv_order must be 2 (got %d)", pr->deriv_order);
+  if (pr->batch < 1) return set_err(MPDE_ERR_INVALID_ARG, "batch must be >= 1");
+  long long P = 1;
+  for (int d = 0; d < pr->ndim; ++d) {
+    if (pr->n[d] < 6)
+      return set_err(MPDE_ERR_SHAPE, "dim %d has %d points; 5-point edge stencils need >= 6", d,
+                     pr->n[d]);
+    if (!(std::isfinite(pr->h[d]) && pr->h[d] > 0))
+      return set_err(MPDE_ERR_INVALID_ARG, "step h[%d] must be finite and > 0", d);
+    P *= pr->n[d];
+  }
+  if (P > (1LL << 30)) return set_err(MPDE_ERR_SHAPE, "grid too large");
+  if (!(pr->w_eq > 0 && pr->w_bnd > 0 && pr->w_deriv > 0 && pr->w_smooth > 0))
+    return set_err(MPDE_ERR_INVALID_ARG, "row-group weights must be > 0");
+  if (op->smoother < 0 || op->smoother > 1)
+    return set_err(MPDE_ERR_UNSUPPORTED, "smoother must be 0 (Jacobi) or 1 (Chebyshev)");
+  if (op->nu < 1 || op->nu > 16) return set_err(MPDE_ERR_INVALID_ARG, "nu must be in 1..16");
+  if (op->max_refine < 1 || op->max_iters < 1 || op->poll_every < 1)
+    return set_err(MPDE_ERR_INVALID_ARG, "max_refine, max_iters, poll_every must be >= 1");
+  if (op->lanczos_steps < 2 || op->lanczos_steps > 32)
+    return set_err(MPDE_ERR_INVALID_ARG, "lanczos_steps must be in 2..32");
+  if (op->precision < 0 || op->precision > 2)
+    return set_err(MPDE_ERR_INVALID_ARG, "precision must be 0, 1 or 2");
+  if (!(op->tol > 0) || !(op->tol_inner > 0))
+    return set_err(MPDE_ERR_INVALID_ARG, "tolerances must be > 0");
+  return MPDE_OK;
+}
+
+// n -> ceil(n/2) for dims with n > coarsest whose half keeps >= 6 points (P:279-280,
+// reading Q10); stop when nothing coarsens, or at levels_max / kMaxLevels.
+int plan_levels(const mpde_problem* pr, const mpde_options* op, LevelShape* lv) {
+  const int D = pr->ndim;
+  int L = 0;
+  LevelShape cur;
+  cur.P = 1;
+  for (int d = 0; d < D; ++d) {
+    cur.n[d] = pr->n[d];
+    cur.P *= cur.n[d];
+  }
+  for (int d = D; d < kMaxD; ++d) cur.n[d] = 1;
+  lv[L++] = cur;
+  const int lmax = std::max(1, std::min(op->levels_max, kMaxLevels));
+  while (L < lmax) {
+    LevelShape nx = cur;
+    bool any = false;
+    nx.P = 1;
+    for (int d = 0; d < D; ++d) {
+      const int h = (cur.n[d] + 1) / 2;
+      if (cur.n[d] > op->coarsest && h >= 6) {
+        nx.n[d] = h;
+        any = true;
+      }
+      nx.P *= nx.n[d];
+    }
+    if (!any) break;
+    lv[L++] = nx;
+    cur = nx;
+  }
+  return L;
+}
+
+constexpr int kMaxCoarse = 1024;  // dense inverse on the coarsest level
+
+Geo make_geo(const mpde_problem* pr, const LevelShape& s, int level_scale[kMaxD]) {
+  Geo G{};
+  G.D = pr->ndim;
+  G.P = s.P;
+  for (int d = 0; d < kMaxD; ++d) {
+    G.n[d] = d < G.D ? s.n[d] : 1;
+  }
+  for (int d = G.D - 1, st = 1; d >= 0; --d) {
+    G.stride[d] = st;
+    st *= G.n[d];
+  }
+  for (int d = 0; d < G.D; ++d) {
+    const double h = pr->h[d] * level_scale[d];
+    G.hd[d] = h;
+    G.h2d[d] = h * h;
+    G.h[d] = float(h);
+    G.h2[d] = float(h * h);
+  }
+  G.we = pr->w_eq;
+  G.wb = pr->w_bnd;
+  G.wr = pr->w_deriv;
+  G.ws = pr->w_smooth;
+  return G;
+}
+
+struct Bump {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+// ---- optional launch profiler (mpde_profile_begin/end): CUDA events around every
+// launch class on the launching stream; off by default (zero cost when off).
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<int> cls;
+  unsigned long long* d_pts = nullptr;  // [8] points processed by k_schur_out per EPI, [8] k_schur_g
+};
+Prof g_prof;
+
+inline void prof_start(cudaStream_t s) {
+  if (!g_prof.on) return;
+  if (g_prof.used + 2 > g_prof.pool.size()) {
+    const size_t n = g_prof.pool.size();
+    g_prof.pool.resize(n + 8192);
+    for (size_t i = n; i < g_prof.pool.size(); ++i) cudaEventCreate(&g_prof.pool[i]);
+  }
+  cudaEventRecord(g_prof.pool[g_prof.used], s);
+}
+inline void prof_stop(int c, cudaStream_t s) {
+  if (!g_prof.on) return;
+  cudaEventRecord(g_prof.pool[g_prof.used + 1], s);
+  g_prof.cls.push_back(c);
+  g_prof.used += 2;
+}
+#define PROF(cls, s, ...)   \
+  do {                      \
+    prof_start(s);          \
+    __VA_ARGS__;            \
+    prof_stop((cls), (s));  \
+  } while (0)
+
+}  // namespace
+
+struct Level {
+  Geo G;
+  int P;
+  const float* c;   // coefficient fields [B][M][P] (level 0: caller's)
+  float* cbuf;      // owned coarse coefficients (levels >= 1)
+  float* dinv;      // [B][P]
+  double* lmax;     // [B]
+  float* coef;      // [B][2 nu]
+  float *r, *e, *d, *d2, *g, *pe;  // [B][P]
+};
+
+struct mpde_hierarchy {
+  mpde_problem prob;
+  mpde_options opts;
+  int B, M, P, L, Pc;
+  Level lv[kMaxLevels];
+  float* sinv;       // [B][Pc][Pc]
+  // PCG on level 0
+  float *x, *rp, *p, *q;
+  // full-system vectors
+  float *rfull, *tfull;
+  double* z64;
+  // build scratch (aliases the full-system region)
+  float *probe_x, *probe_g, *probe_y;
+  double* probe_a;
+  double* part;
+  int part_nt;
+  PdeState st;
+  int* d_count;
+  int* h_count;  // pinned
+  int* ones;     // [B] all 1
+  float* rho;    // [B][P] equation residual b - c.z* of the last forward (fp64-derived)
+  const float* rho_b;  // rhs_b it was computed for
+};
+
+inline bool f64_outer(const mpde_hierarchy* h) { return h->opts.precision >= 1; }
+inline bool f64_vcycle(const mpde_hierarchy* h) { return h->opts.precision >= 2; }
+
+namespace {
+
+// Workspace plan; base == nullptr -> sizing only.
+size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base,
+                      mpde_hierarchy* H) {
+  LevelShape shp[kMaxLevels];
+  const int L = plan_levels(pr, op, shp);
+  const int B = pr->batch, D = pr->ndim, M = 1 + 2 * D;
+  const int P = shp[0].P, Pc = shp[L - 1].P;
+  Bump bp{base};
+  mpde_hierarchy tmp;
+  mpde_hierarchy* h = H ? H : &tmp;
+  int scale[kMaxD] = {1, 1, 1};
+  for (int l = 0; l < L; ++l) {
+    Level& lv = h->lv[l];
+    if (l > 0)
+      for (int d = 0; d < D; ++d)
+        if (shp[l].n[d] != shp[l - 1].n[d]) scale[d] *= 2;
+    lv.G = make_geo(pr, shp[l], scale);
+    lv.P = shp[l].P;
+    lv.cbuf = l > 0 ? bp.take<float>((size_t)B * M * lv.P) : nullptr;
+    lv.dinv = bp.take<float>((size_t)B * lv.P);
+    lv.lmax = bp.take<double>(B);
+    lv.coef = bp.take<float>((size_t)B * 2 * op->nu);
+    lv.r = bp.take<float>((size_t)B * lv.P);
+    lv.e = bp.take<float>((size_t)B * lv.P);
+    lv.d = bp.take<float>((size_t)B * lv.P);
+    lv.d2 = bp.take<float>((size_t)B * lv.P);
+    lv.g = bp.take<float>((size_t)2 * B * lv.P);  // 8 bytes per point (fp64 g)
+    lv.pe = bp.take<float>((size_t)B * lv.P);
+  }
+  h->sinv = bp.take<float>((size_t)B * Pc * Pc);
+  h->x = bp.take<float>((size_t)B * P);
+  h->rp = bp.take<float>((size_t)B * P);
+  h->p = bp.take<float>((size_t)B * P);
+  h->q = bp.take<float>((size_t)B * P);
+  h->part_nt = ntiles(P);
+  h->part = bp.take<double>((size_t)B * h->part_nt + 64);
+  h->st.rz = bp.take<double>(B);
+  h->st.rr0 = bp.take<double>(B);
+  h->st.rhsn = bp.take<double>(B);
+  h->st.relres = bp.take<double>(B);
+  h->st.lmax = nullptr;
+  h->st.alpha = bp.take<float>(B);
+  h->st.beta = bp.take<float>(B);
+  h->st.act = bp.take<int>(B);
+  h->st.done = bp.take<int>(B);
+  h->st.iters = bp.take<int>(B);
+  h->st.pass_iters = bp.take<int>(B);
+  h->st.refines = bp.take<int>(B);
+  h->st.status = bp.take<int>(B);
+  h->st.lz = bp.take<double>((size_t)B * 64);
+  h->rho = bp.take<float>((size_t)B * P);
+  h->st.inpass = bp.take<int>(B);
+  h->st.failed = bp.take<int>(B);
+  h->d_count = bp.take<int>(1);
+  h->ones = bp.take<int>(B);
+  // union: full-system solve vectors | coarsest probing scratch
+  const size_t u0 = bp.off;
+  h->rfull = bp.take<float>((size_t)B * M * P);
+  h->tfull = bp.take<float>((size_t)B * M * P);
+  h->z64 = bp.take<double>((size_t)B * M * P);
+  const size_t u1 = bp.off;
+  bp.off = u0;
+  h->probe_x = bp.take<float>((size_t)B * Pc * Pc);
+  h->probe_g = bp.take<float>((size_t)2 * B * Pc * Pc);
+  h->probe_y = bp.take<float>((size_t)B * Pc * Pc);
+  h->probe_a = bp.take<double>((size_t)B * Pc * Pc);
+  bp.off = std::max(bp.off, u1);
+  h->L = L;
+  h->B = B;
+  h->M = M;
+  h->P = P;
+  h->Pc = Pc;
+  return bp.off + 256;
+}
+
+__global__ void k_fill_int(int n, int* a, int v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+
+PdeState state_with_lmax(const mpde_hierarchy* h, double* lmax) {
+  PdeState s = h->st;
+  s.lmax = lmax;
+  return s;
+}
+
+// S x -> (g scratch, output through epilogue)
+// precision tiers (mpde_options.precision): f64 arithmetic for the PCG operator and
+// the condensation when >= 1, for the V-cycle too when >= 2 (f64_outer / f64_vcycle).
+
+int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const float* x,
+                const EpiArgs& A, const int* act, bool f64, cudaStream_t s) {
+  Level& lv = h->lv[l];
+  EpiArgs A2 = A;
+  A2.pts = g_prof.on ? g_prof.d_pts : nullptr;
+  PROF(0, s, launch_schur_g(lv.G, nvec, crep, lv.c, x, lv.g, act, A2.pts ? A2.pts + 8 : nullptr,
+                            f64, s));
+  PROF(1, s, launch_schur_out(epi, lv.G, nvec, crep, lv.c, x, lv.g, A2, act, f64, s));
+  CKL();
+  return MPDE_OK;
+}
+
+// One V-cycle on level l for rhs `rin` (level 0: PCG residual, copied), writing the
+// correction into lv.e.  rdot/part: optional <rdot, e> partials from the last kernel.
+int vcycle(mpde_hierarchy* h, int l, const float* rin, const float* rdot, double* part,
+           const int* act, cudaStream_t s) {
+  const int B = h->B;
+  Level& lv = h->lv[l];
+  const int nu = h->opts.nu;
+  if (l == h->L - 1) {
+    PROF(8, s, launch_coarse_gemv(lv.P, B, h->sinv, rin, lv.e, rdot, part, act, s));
+    CKL();
+    return MPDE_OK;
+  }
+  Level& lc = h->lv[l + 1];
+  EpiArgs A;
+  A.dinv = lv.dinv;
+  A.coef = lv.coef;
+  A.coef_stride = 2 * nu;
+  A.res = lv.r;
+  A.e = lv.e;
+  // pre-smoothing from e = 0: d0 = beta0 Dinv r, e = d0, res = r
+  PROF(6, s, launch_smooth_start(lv.P, B, rin, lv.dinv, lv.coef, 2 * nu, lv.r, lv.d, lv.e, act, s));
+  float* dcur = lv.d;
+  float* dnext = lv.d2;
+  for (int k = 1; k < nu; ++k) {
+    A.step = k;
+    A.d_out = dnext;
+    if (int rc = schur_apply(h, l, EPI_SMOOTH, B, 1, dcur, A, act, f64_vcycle(h), s)) return rc;
+    std::swap(dcur, dnext);
+  }
+  // residual after pre-smoothing, restrict
+  if (int rc = schur_apply(h, l, EPI_RESID, B, 1, dcur, A, act, f64_vcycle(h), s)) return rc;
+  PROF(5, s, launch_restrict(lv.G, lc.G, B, 1, lv.r, lc.r, act, 1, s));
+  CKL();
+  if (int rc = vcycle(h, l + 1, lc.r, nullptr, nullptr, act, s)) return rc;
+  PROF(5, s, launch_prolong(lv.G, lc.G, B, lc.e, lv.pe, act, s));
+  CKL();
+  // post-smoothing: e += P e_c; res -= S (P e_c); d0 = beta0 Dinv res; e += d0
+  A.step = 0;
+  A.d_out = lv.d;
+  A.rdot = nu == 1 ? rdot : nullptr;
+  A.part = nu == 1 ? part : nullptr;
+  if (int rc = schur_apply(h, l, EPI_POST0, B, 1, lv.pe, A, act, f64_vcycle(h), s)) return rc;
+  dcur = lv.d;
+  dnext = lv.d2;
+  for (int k = 1; k < nu; ++k) {
+    const bool last = (k == nu - 1);
+    A.step = k;
+    A.d_out = dnext;
+    A.rdot = last ? rdot : nullptr;
+    A.part = last ? part : nullptr;
+    if (int rc = schur_apply(h, l, last ? EPI_SMOOTH_LAST : EPI_SMOOTH, B, 1, dcur, A, act,
+                               f64_vcycle(h), s))
+      return rc;
+    std::swap(dcur, dnext);
+  }
+  return MPDE_OK;
+}
+
+int poll_active(mpde_hierarchy* h, cudaStream_t s, int* nact) {
+  PROF(7, s, launch_count_active(h->B, h->st.act, h->d_count, s));
+  CKL();
+  CK(cudaMemcpyAsync(h->h_count, h->d_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *nact = *h->h_count;
+  return MPDE_OK;
+}
+
+// k_dot partial for rr0: reuse pcg_update with alpha = 0 would touch p; use a dedicated path
+__global__ void k_dot_self(int P, const float* __restrict__ r, double* part, const int* act) {
+  const int v = blockIdx.y;
+  if (act && !act[v]) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  double d = 0.0;
+  if (p < P) {
+    const float x = r[(size_t)v * P + p];
+    d = double(x) * x;
+  }
+  d = block_sum(d);
+  if (threadIdx.x == 0) part[(size_t)v * gridDim.x + blockIdx.x] = d;
+}
+
+// PCG on the condensed system S x = rp (level 0), x0 = 0.
+int pcg(mpde_hierarchy* h, cudaStream_t s) {
+  const int B = h->B, P = h->P;
+  const int nt = ntiles(P);
+  const int ntc = h->L == 1 ? coarse_gemv_blocks(h->Pc) : nt;
+  const float tol2 = h->opts.tol_inner * h->opts.tol_inner;
+  const int* act = h->st.act;
+  Level& l0 = h->lv[0];
+  CK(cudaMemsetAsync(h->x, 0, sizeof(float) * (size_t)B * P, s));
+  ++g_launch_count;
+  PROF(6, s, k_dot_self<<<dim3(nt, B), kThreads, 0, s>>>(P, h->rp, h->part, act));
+  CKL();
+  PROF(7, s, launch_scalar(SC_INIT, B, h->st, h->part, nt, tol2, h->opts.max_iters, s));
+  if (int rc = vcycle(h, 0, h->rp, h->rp, h->part, act, s)) return rc;
+  PROF(7, s, launch_scalar(SC_RZ0, B, h->st, h->part, ntc, tol2, h->opts.max_iters, s));
+  PROF(6, s, launch_p_update(P, B, h->st.beta, l0.e, h->p, act, s));
+  CKL();
+  for (int it = 0; it < h->opts.max_iters; ++it) {
+    EpiArgs A;
+    A.y = h->q;
+    A.part = h->part;
+    if (int rc = schur_apply(h, 0, EPI_DOT, B, 1, h->p, A, act, f64_outer(h), s)) return rc;
+    PROF(7, s, launch_scalar(SC_ALPHA, B, h->st, h->part, nt, tol2, h->opts.max_iters, s));
+    PROF(6, s, launch_pcg_update(P, B, h->st.alpha, h->p, h->q, h->x, h->rp, h->part, act, s));
+    PROF(7, s, launch_scalar(SC_CONV, B, h->st, h->part, nt, tol2, h->opts.max_iters, s));
+    CKL();
+    if ((it + 1) % h->opts.poll_every == 0 || it + 1 == h->opts.max_iters) {
+      int nact = 0;
+      if (int rc = poll_active(h, s, &nact)) return rc;
+      if (nact == 0) break;
+    }
+    if (int rc = vcycle(h, 0, h->rp, h->rp, h->part, act, s)) return rc;
+    PROF(7, s, launch_scalar(SC_BETA, B, h->st, h->part, ntc, tol2, h->opts.max_iters, s));
+    PROF(6, s, launch_p_update(P, B, h->st.beta, l0.e, h->p, act, s));
+    CKL();
+  }
+  return MPDE_OK;
+}
+
+// Solve N z = rhs for every PDE (refinement loop); result in h->z64.  rhs == nullptr:
+// rhs = A^T d from (b, om), formed in fp64 inside the residual kernel.
+int solve_core(mpde_hierarchy* h, const float* rhs, const float* b, const float* om,
+               cudaStream_t s) {
+  const int B = h->B, P = h->P, M = h->M;
+  const int nt = ntiles(P);
+  Level& l0 = h->lv[0];
+  CK(cudaMemsetAsync(h->z64, 0, sizeof(double) * (size_t)B * M * P, s));
+  PROF(2, s, launch_residual64(l0.G, B, l0.c, rhs, b, om, nullptr, h->rfull, h->part, nullptr, s));
+  PROF(7, s, launch_scalar(SC_RHSNORM, B, h->st, h->part, nt, 0.f, 0, s));
+  CKL();
+  for (int pass = 0; pass < h->opts.max_refine; ++pass) {
+    PROF(7, s, launch_scalar(SC_PASS_BEGIN, B, h->st, h->part, nt, 0.f, 0, s));
+    int nact = 0;
+    if (int rc = poll_active(h, s, &nact)) return rc;
+    if (nact == 0) break;
+    PROF(3, s, launch_ndd_solve(l0.G, B, l0.c, h->rfull, h->tfull, h->st.act, f64_outer(h), s));
+    PROF(3, s, launch_schur_rhs(l0.G, B, l0.c, h->rfull, h->tfull, h->rp, h->st.act, f64_outer(h), s));
+    CKL();
+    if (int rc = pcg(h, s)) return rc;
+    // re-activate every PDE still being refined (PCG deactivated converged ones)
+    PROF(7, s, launch_scalar(SC_REACT, B, h->st, h->part, nt, 0.f, 0, s));
+    PROF(4, s, launch_backsub(l0.G, B, l0.c, h->rfull, h->x, h->z64, h->st.act, f64_outer(h), s));
+    PROF(2, s, launch_residual64(l0.G, B, l0.c, rhs, b, om, h->z64, h->rfull, h->part, h->st.act, s));
+    PROF(7, s, launch_scalar(SC_REFRES, B, h->st, h->part, nt, 0.f, 0, s));
+    CKL();
+  }
+  return MPDE_OK;
+}
+
+}  // namespace
+
+// ==================================================================================
+// C ABI
+// ==================================================================================
+extern "C" {
+
+mpde_options mpde_default_options(void) {
+  mpde_options o;
+  o.tol = 1e-7f;
+  o.tol_inner = 1e-4f;
+  o.max_iters = 500;
+  o.max_refine = 6;
+  o.smoother = 1;
+  o.nu = 2;
+  o.coarsest = 8;
+  o.levels_max = 8;
+  o.poll_every = 8;
+  o.jacobi_theta = 1.3f;
+  o.cheb_ratio = 30.f;
+  o.lanczos_steps = 16;
+  o.precision = 1;
+  return o;
+}
+
+const char* mpde_last_error(void) { return g_err.c_str(); }
+
+int mpde_sizes(const mpde_problem* prob, const mpde_options* opts, int64_t* n_v, int64_t* n_c,
+               int32_t* n_levels) {
+  mpde_options dflt = mpde_default_options();
+  if (!opts) opts = &dflt;
+  if (int rc = validate(prob, opts)) return rc;
+  const int D = prob->ndim;
+  int64_t P = 1;
+  for (int d = 0; d < D; ++d) P *= prob->n[d];
+  int64_t interior = 1;
+  for (int d = 0; d < D; ++d) interior *= (prob->n[d] - 2);
+  int64_t smooth = 0;
+  for (int d = 0; d < D; ++d) smooth += 2 * (int64_t)(prob->n[d] - 1) * (P / prob->n[d]);
+  if (n_v) *n_v = (1 + 2 * D) * P;
+  if (n_c) *n_c = P + (P - interior) + 2 * D * P + smooth;
+  LevelShape shp[kMaxLevels];
+  if (n_levels) *n_levels = plan_levels(prob, opts, shp);
+  return MPDE_OK;
+}
+
+size_t mpde_workspace_bytes(const mpde_problem* prob, const mpde_options* opts) {
+  if (validate(prob, opts)) return 0;
+  return plan_workspace(prob, opts, nullptr, nullptr);
+}
+
+int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, const float* coeff,
+                         void* workspace, size_t workspace_bytes, mpde_stream_t stream_,
+                         mpde_hierarchy** out) {
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (int rc = validate(prob, opts)) return rc;
+  if (!coeff || !workspace || !out) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  const size_t need = plan_workspace(prob, opts, nullptr, nullptr);
+  if (workspace_bytes < need)
+    return set_err(MPDE_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes,
+                   need);
+  upload_constants();
+  mpde_hierarchy* h = new mpde_hierarchy();
+  h->prob = *prob;
+  h->opts = *opts;
+  plan_workspace(prob, opts, (char*)workspace, h);
+  if (h->Pc > kMaxCoarse) {
+    delete h;
+    return set_err(MPDE_ERR_UNSUPPORTED,
+                   "coarsest level has %d points (> %d); raise levels_max / lower coarsest",
+                   h->Pc, kMaxCoarse);
+  }
+  if (cudaHostAlloc(&h->h_count, sizeof(int), cudaHostAllocDefault) != cudaSuccess) {
+    delete h;
+    return set_err(MPDE_ERR_CUDA, "cudaHostAlloc failed");
+  }
+  h->st.tol = opts->tol;
+  const int B = h->B, M = h->M, L = h->L;
+  g_launch_count += 2;
+  k_fill_int<<<(B + 255) / 256, 256, 0, s>>>(B, h->ones, 1);
+  k_fill_int<<<(B + 255) / 256, 256, 0, s>>>(B, h->st.act, 1);
+  h->lv[0].c = coeff;
+  for (int l = 1; l < L; ++l) {
+    // coarse coefficients by full weighting (reading Q11)
+    launch_restrict(h->lv[l - 1].G, h->lv[l].G, B, M, h->lv[l - 1].c, h->lv[l].cbuf, nullptr, 1,
+                    s);
+    h->lv[l].c = h->lv[l].cbuf;
+  }
+  CKL();
+  for (int l = 0; l < L; ++l) {
+    Level& lv = h->lv[l];
+    launch_diag_schur(lv.G, B, lv.c, lv.dinv, s);
+    CKL();
+    if (l == L - 1) break;
+    // lambda_max(D^-1 S) per PDE: Lanczos in the D-inner product (D = diag S), then the
+    // largest Ritz value of the tridiagonal by bisection.
+    PdeState sl = state_with_lmax(h, lv.lmax);
+    const int nt = ntiles(lv.P);
+    float* v = lv.d;
+    float* vp = lv.pe;
+    float* y = lv.d2;
+    launch_rand_fill(lv.P, B, v, 12345u + l, s);
+    CK(cudaMemsetAsync(vp, 0, sizeof(float) * (size_t)B * lv.P, s));
+    launch_scalar(SC_LZ_RESET, B, sl, h->part, nt, 0.f, 0, s);
+    launch_lz_update(lv.P, B, v, v, v, lv.dinv, h->st.alpha, h->st.beta, h->part, s);
+    launch_scalar(SC_LZ_BETA, B, sl, h->part, nt, 0.f, -1, s);
+    launch_scale(lv.P, B, h->st.alpha, v, v, h->ones, s);
+    for (int j = 0; j < opts->lanczos_steps; ++j) {
+      EpiArgs A;
+      A.y = y;
+      A.dinv = lv.dinv;
+      A.part = h->part;
+      if (int rc = schur_apply(h, l, EPI_POWER, B, 1, v, A, h->ones, f64_vcycle(h), s)) {
+        delete h;
+        return rc;
+      }
+      launch_scalar(SC_LZ_ALPHA, B, sl, h->part, nt, 0.f, j, s);
+      launch_lz_update(lv.P, B, y, v, vp, lv.dinv, h->st.alpha, h->st.beta, h->part, s);
+      launch_scalar(SC_LZ_BETA, B, sl, h->part, nt, 0.f, j, s);
+      launch_scale(lv.P, B, h->st.alpha, vp, vp, h->ones, s);
+      std::swap(v, vp);
+    }
+    launch_scalar(SC_LZ_EIG, B, sl, h->part, nt, 0.f, opts->lanczos_steps, s);
+    launch_smooth_coef(B, opts->nu, opts->smoother, opts->jacobi_theta, opts->cheb_ratio, lv.lmax,
+                       lv.coef, s);
+    CKL();
+  }
+  // coarsest level: probe S_c column by column, invert (fp64 Gauss-Jordan)
+  {
+    Level& lc = h->lv[L - 1];
+    const int Pc = lc.P;
+    // grid.y <= 65535: probe in chunks of PDEs
+    const int chunk = std::max(1, 65535 / Pc);
+    for (int b0 = 0; b0 < B; b0 += chunk) {
+      const int nb = std::min(chunk, B - b0);
+      const size_t vo = (size_t)b0 * Pc * Pc;
+      const float* cc = lc.c + (size_t)b0 * M * Pc;
+      launch_identity(Pc, nb * Pc, h->probe_x + vo, s);
+      launch_schur_g(lc.G, nb * Pc, Pc, cc, h->probe_x + vo, h->probe_g + 2 * vo, nullptr, nullptr,
+                     f64_outer(h), s);
+      EpiArgs A;
+      A.y = h->probe_y + vo;
+      launch_schur_out(EPI_STORE, lc.G, nb * Pc, Pc, cc, h->probe_x + vo, h->probe_g + 2 * vo, A,
+                       nullptr, f64_outer(h), s);
+    }
+    launch_coarse_invert(Pc, B, h->probe_y, h->probe_a, h->sinv, s);
+    CKL();
+  }
+  *out = h;
+  return MPDE_OK;
+}
+
+int mpde_destroy_hierarchy(mpde_hierarchy* h) {
+  if (!h) return MPDE_OK;
+  if (h->h_count) cudaFreeHost(h->h_count);
+  delete h;
+  return MPDE_OK;
+}
+
+int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, float* z,
+                   mpde_stats* stats, mpde_stream_t stream_) {
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (!h || !rhs_b || !bnd || !z) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  const int B = h->B;
+  if (int rc = solve_core(h, nullptr, rhs_b, bnd, s)) return rc;
+  PROF(10, s, launch_fwd_out(h->lv[0].G, B, h->lv[0].c, rhs_b, h->z64, z, h->rho, s));
+  h->rho_b = rhs_b;
+  if (stats) launch_stats_out(B, h->st, stats, s);
+  CKL();
+  return MPDE_OK;
+}
+
+int mpde_solve_bwd(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,
+                   float* grad_coeff, float* grad_rhs, float* grad_bnd, float* dz_opt,
+                   mpde_stats* stats, mpde_stream_t stream_) {
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (!h || !rhs_b || !z || !g_z || !grad_coeff || !grad_rhs || !grad_bnd)
+    return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  const int B = h->B;
+  Level& l0 = h->lv[0];
+  if (int rc = solve_core(h, g_z, nullptr, nullptr, s)) return rc;
+  PROF(10, s, launch_grad(l0.G, B, l0.c, rhs_b, z, h->rho_b == rhs_b ? h->rho : nullptr, h->z64,
+                          grad_coeff, grad_rhs, grad_bnd, dz_opt, s));
+  if (stats) launch_stats_out(B, h->st, stats, s);
+  CKL();
+  return MPDE_OK;
+}
+
+int mpde_apply_normal(const mpde_problem* prob, const float* coeff, const float* z, float* q,
+                      mpde_stream_t stream_) {
+  mpde_options o = mpde_default_options();
+  if (int rc = validate(prob, &o)) return rc;
+  if (!coeff || !z || !q) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  upload_constants();
+  LevelShape shp[kMaxLevels];
+  o.levels_max = 1;
+  plan_levels(prob, &o, shp);
+  int scale[kMaxD] = {1, 1, 1};
+  Geo G = make_geo(prob, shp[0], scale);
+  launch_apply_normal(G, prob->batch, coeff, z, q, (cudaStream_t)stream_);
+  CKL();
+  return MPDE_OK;
+}
+
+int mpde_apply_schur(mpde_hierarchy* h, int32_t level, const float* x, float* y,
+                     mpde_stream_t stream_) {
+  if (!h || !x || !y) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  if (level < 0 || level >= h->L) return set_err(MPDE_ERR_INVALID_ARG, "bad level %d", level);
+  EpiArgs A;
+  A.y = y;
+  return schur_apply(h, level, EPI_STORE, h->B, 1, x, A, nullptr, f64_outer(h),
+                     (cudaStream_t)stream_);
+}
+
+int mpde_apply_precond(mpde_hierarchy* h, const float* r, float* z, mpde_stream_t stream_) {
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (!h || !r || !z) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  if (int rc = vcycle(h, 0, r, nullptr, nullptr, h->ones, s)) return rc;
+  CK(cudaMemcpyAsync(z, h->lv[0].e, sizeof(float) * (size_t)h->B * h->P, cudaMemcpyDeviceToDevice,
+                     s));
+  return MPDE_OK;
+}
+
+int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* dst,
+                         mpde_stream_t stream_) {
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (!h || !dst) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  if (level < 0 || level >= h->L) return set_err(MPDE_ERR_INVALID_ARG, "bad level %d", level);
+  const Level& lv = h->lv[level];
+  const int B = h->B;
+  switch (what) {
+    case 0: {
+      int32_t shp[4] = {lv.G.n[0], lv.G.n[1], h->prob.ndim > 2 ? lv.G.n[2] : 0, h->L};
+      std::memcpy(dst, shp, sizeof(shp));
+      return MPDE_OK;
+    }
+    case 1:
+      CK(cudaMemcpyAsync(dst, lv.dinv, sizeof(float) * (size_t)B * lv.P, cudaMemcpyDeviceToDevice, s));
+      return MPDE_OK;
+    case 2:
+      launch_d2f(B, lv.lmax, (float*)dst, s);
+      CKL();
+      return MPDE_OK;
+    case 3:
+      CK(cudaMemcpyAsync(dst, lv.c, sizeof(float) * (size_t)B * h->M * lv.P, cudaMemcpyDeviceToDevice, s));
+      return MPDE_OK;
+    case 4:
+      CK(cudaMemcpyAsync(dst, h->sinv, sizeof(float) * (size_t)B * h->Pc * h->Pc,
+                         cudaMemcpyDeviceToDevice, s));
+      return MPDE_OK;
+  }
+  return set_err(MPDE_ERR_INVALID_ARG, "unknown query %d", what);
+}
+
+uint64_t mpde_launch_count(void) { return g_launch_count; }
+
+int mpde_profile_begin(void) {
+  if (!g_prof.d_pts) CK(cudaMalloc(&g_prof.d_pts, 16 * sizeof(unsigned long long)));
+  CK(cudaMemset(g_prof.d_pts, 0, 16 * sizeof(unsigned long long)));
+  g_prof.used = 0;
+  g_prof.cls.clear();
+  g_prof.on = true;
+  return MPDE_OK;
+}
+
+int mpde_profile_end(double* ms, int64_t* launches, uint64_t* pts) {
+  if (!g_prof.on) return set_err(MPDE_ERR_INVALID_ARG, "profiler not running");
+  g_prof.on = false;
+  for (int c = 0; c < MPDE_PROF_NCLASS; ++c) {
+    if (ms) ms[c] = 0.0;
+    if (launches) launches[c] = 0;
+  }
+  if (g_prof.used) CK(cudaEventSynchronize(g_prof.pool[g_prof.used - 1]));
+  for (size_t i = 0; i < g_prof.cls.size(); ++i) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, g_prof.pool[2 * i], g_prof.pool[2 * i + 1]));
+    const int c = g_prof.cls[i];
+    if (ms) ms[c] += t;
+    if (launches) launches[c] += 1;
+  }
+  if (pts) {
+    unsigned long long h[16];
+    CK(cudaMemcpy(h, g_prof.d_pts, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 16; ++i) pts[i] = h[i];
+  }
+  return MPDE_OK;
+}
+
+int mpde_batch_sum(const float* x, int32_t batch, int64_t n, float* out, mpde_stream_t stream_) {
+  if (!x || !out || batch < 1 || n < 0) return set_err(MPDE_ERR_INVALID_ARG, "bad batch_sum args");
+  launch_batch_sum(x, batch, n, out, (cudaStream_t)stream_);
+  CKL();
+  return MPDE_OK;
+}
+
+size_t mpde_host_staging_bytes(const mpde_problem* prob) {
+  mpde_options o = mpde_default_options();
+  if (validate(prob, &o)) return 0;
+  size_t P = 1;
+  for (int d = 0; d < prob->ndim; ++d) P *= prob->n[d];
+  const size_t B = prob->batch, M = 1 + 2 * prob->ndim;
+  // c, g, z, grad_c: B*M*P each; b, omega, grad_b, grad_omega: B*P each
+  return sizeof(float) * (4 * B * M * P + 4 * B * P) + 8 * 256;
+}
+
+int mpde_fwd_bwd_host(const mpde_problem* prob, const mpde_options* opts, const float* coeff_h,
+                      const float* rhs_h, const float* bnd_h, const float* gz_h, float* z_h,
+                      float* grad_coeff_h, float* grad_rhs_h, float* grad_bnd_h,
+                      void* device_staging, void* workspace, size_t workspace_bytes,
+                      mpde_stream_t stream_) {
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (int rc = validate(prob, opts)) return rc;
+  if (!coeff_h || !rhs_h || !bnd_h || !gz_h || !z_h || !grad_coeff_h || !grad_rhs_h ||
+      !grad_bnd_h || !device_staging)
+    return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  size_t P = 1;
+  for (int d = 0; d < prob->ndim; ++d) P *= prob->n[d];
+  const size_t B = prob->batch, M = 1 + 2 * prob->ndim;
+  Bump bp{(char*)device_staging};
+  float* c = bp.take<float>(B * M * P);
+  float* g = bp.take<float>(B * M * P);
+  float* z = bp.take<float>(B * M * P);
+  float* gc = bp.take<float>(B * M * P);
+  float* b = bp.take<float>(B * P);
+  float* om = bp.take<float>(B * P);
+  float* gb = bp.take<float>(B * P);
+  float* gw = bp.take<float>(B * P);
+  CK(cudaMemcpyAsync(c, coeff_h, sizeof(float) * B * M * P, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(b, rhs_h, sizeof(float) * B * P, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(om, bnd_h, sizeof(float) * B * P, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(g, gz_h, sizeof(float) * B * M * P, cudaMemcpyHostToDevice, s));
+  mpde_hierarchy* h = nullptr;
+  if (int rc = mpde_build_hierarchy(prob, opts, c, workspace, workspace_bytes, stream_, &h))
+    return rc;
+  int rc = mpde_solve_fwd(h, b, om, z, nullptr, stream_);
+  if (!rc) rc = mpde_solve_bwd(h, b, z, g, gc, gb, gw, nullptr, nullptr, stream_);
+  mpde_destroy_hierarchy(h);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(z_h, z, sizeof(float) * B * M * P, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(grad_coeff_h, gc, sizeof(float) * B * M * P, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(grad_rhs_h, gb, sizeof(float) * B * P, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(grad_bnd_h, gw, sizeof(float) * B * P, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return MPDE_OK;
+}
+
+}  // extern "C"

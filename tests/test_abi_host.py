@@ -1,0 +1,73 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/mpde.h
+declares, and its host logic (validation, sizes, level plan) agrees with the oracle's
+counts -- no compute calls (no GPU here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from oracle import counts
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def mp():
+    from paper_2502_18377_b200 import build, mpde
+    build.build()
+    return mpde
+
+
+def test_exports_every_declared_symbol(mp):
+    hdr = open(os.path.join(ROOT, "include", "mpde.h")).read()
+    declared = set(re.findall(r"\b(mpde_[a-z_0-9]+)\s*\(", hdr))
+    assert declared >= {"mpde_build_hierarchy", "mpde_solve_fwd", "mpde_solve_bwd"}
+    lib = C.CDLL(mp.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(mp.EXPORTS)
+
+
+@pytest.mark.parametrize("shape", [(16, 16), (32, 32), (101, 256), (32, 32, 32), (32, 64, 64)])
+def test_sizes_match_oracle_counts(mp, shape):
+    prob = mp.make_problem(shape, [0.1] * len(shape), 4)
+    n_v, n_c, _ = mp.mpde_sizes(prob)
+    assert (n_v, n_c) == counts(shape)
+
+
+def test_level_plan(mp):
+    """halve each dim (ceil, keeping >= 6 points) down to size 8."""
+    cases = {(32, 64, 64): 4, (101, 256): 6, (16, 16): 2, (32, 32, 32): 3, (64, 128, 128): 5}
+    for shape, L in cases.items():
+        prob = mp.make_problem(shape, [0.1] * len(shape), 1)
+        assert mp.mpde_sizes(prob)[2] == L, shape
+    prob = mp.make_problem((32, 64, 64), [0.1] * 3, 1)
+    assert mp.mpde_sizes(prob, mp.mpde_default_options(levels_max=2))[2] == 2
+
+
+def test_validation_errors(mp):
+    lib = mp.lib()
+    bad = [mp.make_problem((5, 16), (0.1, 0.1), 1),            # n < 6 (Q4)
+           mp.make_problem((16, 16), (0.0, 0.1), 1),           # h = 0
+           mp.make_problem((16, 16), (0.1, 0.1), 0)]           # batch 0
+    codes = []
+    for pr in bad:
+        codes.append(lib.mpde_sizes(C.byref(pr), None, None, None, None))
+    assert codes == [2, 1, 1]
+    assert "6" in lib.mpde_last_error().decode() or lib.mpde_last_error()
+    pr = mp.make_problem((16, 16), (0.1, 0.1), 1)
+    pr.deriv_order = 3
+    assert lib.mpde_sizes(C.byref(pr), None, None, None, None) == 3
+    opts = mp.mpde_default_options(smoother=7)
+    assert lib.mpde_workspace_bytes(C.byref(mp.make_problem((16, 16), (0.1, 0.1), 1)),
+                                    C.byref(opts)) == 0
+
+
+def test_workspace_scales_linearly_in_batch(mp):
+    o = mp.mpde_default_options()
+    w1 = mp.mpde_workspace_bytes(mp.make_problem((32, 64, 64), (0.01, 1 / 64, 1 / 64), 1), o)
+    w32 = mp.mpde_workspace_bytes(mp.make_problem((32, 64, 64), (0.01, 1 / 64, 1 / 64), 32), o)
+    assert 30 * w1 < w32 < 33 * w1
+    # ~ tens of bytes per unknown (matrix-free), far below a CSR A^T A
+    assert w32 / (32 * 7 * 131072) < 80

@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs.  Tolerances from BASELINE.json north_star: relative L2 solution error <= 1e-4,
+relative gradient error <= 1e-3 (SURVEY.md §8(c) "Parity definitions")."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import Problem, assemble, boundary_mask, solve_backward, solve_forward
+
+pytestmark = pytest.mark.gpu
+
+E_Z, E_G = 1e-4, 1e-3
+
+
+def _rand_problem(shape, B, seed):
+    rng = np.random.default_rng(seed)
+    D = len(shape)
+    M, P = 1 + 2 * D, int(np.prod(shape))
+    c = rng.normal(0.0, 0.5, (B, M, P))
+    c[:, 1] += 1.0
+    b = rng.normal(size=(B, P))
+    om = rng.normal(size=(B, P))
+    g = rng.normal(size=(B, M, P))
+    f32 = lambda a: a.astype(np.float32)
+    return f32(c), f32(b), f32(om), f32(g)
+
+
+def _oracle(shape, h, c, b, om, g, weights=(1, 1, 1, 1), method="auto"):
+    pr = Problem(tuple(shape), tuple(h), *weights)
+    outs = []
+    for i in range(c.shape[0]):
+        f = solve_forward(pr, c[i], b[i], om[i], method=method)
+        bw = solve_backward(pr, f, g[i].reshape(-1).astype(np.float64), method=method) \
+            if g is not None else None
+        outs.append((f, bw))
+    return pr, outs
+
+
+@pytest.fixture(scope="module")
+def gu():
+    import gpu_util
+    return gpu_util
+
+
+# ----------------------------------------------------------------- operator parity (K1)
+@pytest.mark.parametrize("shape,h", [((16, 16), (1 / 15, 1 / 15)), ((8, 9, 10), (0.1, 0.07, 0.05)),
+                                     ((6, 7, 11), (0.3, 0.2, 0.1))])
+def test_normal_apply_matches_oracle_csr(shape, h, gu):
+    """P10: N p = A^T (A p) against the oracle's explicit CSR, several tiles + ragged tail."""
+    from paper_2502_18377_b200 import mpde
+    B = 3
+    c, _, _, _ = _rand_problem(shape, B, 11)
+    rng = np.random.default_rng(12)
+    z = rng.normal(size=c.shape).astype(np.float32)
+    w = (1.25, 2.0, 0.75, 0.875)  # exactly representable in fp32 (the ABI takes float weights)
+    prob = mpde.make_problem(shape, h, B, *w)
+    q = torch.empty_like(gu.to_dev(z))
+    mpde.mpde_apply_normal(prob, gu.to_dev(c), gu.to_dev(z), q)
+    q = q.cpu().numpy().astype(np.float64)
+    pr = Problem(shape, h, *w)
+    for i in range(B):
+        A, _, _ = assemble(pr, c[i], np.zeros(pr.P), np.zeros(pr.P))
+        ref = A.T @ (A @ z[i].reshape(-1).astype(np.float64))
+        assert gu.rel(q[i], ref) <= 1e-6
+
+
+def _dense_schur(pr, c):
+    A, _, _ = assemble(pr, c, np.zeros(pr.P), np.zeros(pr.P))
+    N = (A.T @ A).toarray()
+    P = pr.P
+    Npp, Npd, Ndd = N[:P, :P], N[:P, P:], N[P:, P:]
+    return Npp - Npd @ np.linalg.solve(Ndd, Npd.T)
+
+
+@pytest.mark.parametrize("shape,h", [((12, 10), (0.1, 0.05)), ((7, 8, 9), (0.1, 0.2, 0.15))])
+def test_schur_apply_and_diag(shape, h, gu):
+    """The condensed operator S (block elimination of the derivative variables) and its
+    diagonal, against S computed densely from the oracle's A."""
+    from paper_2502_18377_b200 import mpde
+    B = 2
+    c, b, om, _ = _rand_problem(shape, B, 21)
+    w = (1.25, 2.0, 0.75, 0.875)  # exactly representable in fp32 (the ABI takes float weights)
+    opts = mpde.mpde_default_options(levels_max=1)
+    s = mpde.Solver(shape, h, gu.to_dev(c), opts=opts, weights=w)
+    rng = np.random.default_rng(22)
+    x = rng.normal(size=(B, s.P)).astype(np.float32)
+    y = torch.empty((B, s.P), dtype=torch.float32, device="cuda")
+    mpde.mpde_apply_schur(s.h_, 0, gu.to_dev(x), y)
+    dinv = torch.empty_like(y)
+    mpde.mpde_hierarchy_query(s.h_, 0, 1, dinv)
+    sinv = torch.empty((B, s.P, s.P), dtype=torch.float32, device="cuda")
+    mpde.mpde_hierarchy_query(s.h_, 0, 4, sinv)
+    torch.cuda.synchronize()
+    pr = Problem(shape, h, *w)
+    for i in range(B):
+        S = _dense_schur(pr, c[i].astype(np.float64))
+        assert gu.rel(y[i].cpu().numpy(), S @ x[i]) <= 1e-4
+        assert gu.rel(1.0 / dinv[i].cpu().numpy(), np.diag(S)) <= 1e-5
+        assert gu.rel(sinv[i].cpu().numpy() @ S, np.eye(s.P)) <= 1e-3
+    s.close()
+
+
+# ----------------------------------------------------------------- forward / backward
+@pytest.mark.parametrize("shape,h,B", [((16, 16), (1 / 15, 1 / 15), 2), ((20, 26), (0.05, 0.04), 3),
+                                       ((10, 12, 14), (0.1, 0.08, 0.07), 2)])
+def test_fwd_bwd_random_problems(shape, h, B, gu):
+    c, b, om, g = _rand_problem(shape, B, 31)
+    w = (1.25, 2.0, 0.75, 0.875)  # exactly representable in fp32 (the ABI takes float weights)
+    out = gu.gpu_solve(shape, h, c, b, om, g, weights=w)
+    pr, ref = _oracle(shape, h, c, b, om, g, weights=w,
+                      method="dense" if np.prod(shape) * (1 + 2 * len(shape)) <= 5000 else "lu")
+    bm = boundary_mask(shape)
+    for i in range(B):
+        f, bw = ref[i]
+        assert out["stats_fwd"][i]["status"] == "converged", out["stats_fwd"][i]
+        assert gu.rel(out["z"][i], f["z"]) <= E_Z
+        assert gu.rel(out["grad_c"][i], bw["grad_c"]) <= E_G
+        assert gu.rel(out["grad_b"][i], bw["grad_b"]) <= E_G
+        assert gu.rel(out["grad_omega"][i], bw["grad_omega"]) <= E_G
+        assert np.all(out["grad_omega"][i][~bm] == 0.0)
+
+
+def test_c1_heat_parity(gu):
+    """C1 (BASELINE configs[0]): 1D heat 16x16, batch 1, oracle dense SVD lstsq; both loss
+    directions of SURVEY §8(c) (random g, and g = u_phi - u_ref on phi slots)."""
+    bt = synth.make_batch("C1")
+    cfg = bt["cfg"]
+    g1 = synth.make_g("C1")
+    pr = Problem(cfg.shape, cfg.h)
+    f = solve_forward(pr, bt["c"][0], bt["b"][0], bt["omega"][0], method="dense")
+    g2 = np.zeros_like(g1)
+    g2[0, 0] = (f["z"][:pr.P] - bt["omega"][0]).astype(np.float32)
+    for g in (g1, g2):
+        out = gu.gpu_solve(cfg.shape, cfg.h, bt["c"], bt["b"], bt["omega"], g)
+        bw = solve_backward(pr, f, g[0].reshape(-1).astype(np.float64), method="dense")
+        assert gu.rel(out["z"][0], f["z"]) <= E_Z
+        for k in ("grad_c", "grad_b", "grad_omega"):
+            assert gu.rel(out[k][0], bw[k]) <= E_G, k
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_mms_full_size(name, gu):
+    """P2 at the configs' full sizes (C4 = the bench workload, full batch): the closed-form
+    manufactured solution is recovered within 1e-4 by the CUDA path."""
+    m = synth.make_mms(name)
+    cfg = m["cfg"]
+    out = gu.gpu_solve(cfg.shape, cfg.h, m["c"], m["b"], m["omega"])
+    errs = [gu.rel(out["z"][i], m["z_exact"][i]) for i in range(m["c"].shape[0])]
+    its = [s["iters"] for s in out["stats_fwd"]]
+    print(name, "max e_z", max(errs), "iters", min(its), max(its))
+    assert max(errs) <= E_Z
+    assert all(s["status"] == "converged" for s in out["stats_fwd"])
+
+
+def test_c2_sampled_parity(gu):
+    """C2 (Burgers template, 256x101): PDEs 0 and 1 against the oracle (SuperLU)."""
+    bt = synth.make_batch("C2", batch=2)
+    cfg = bt["cfg"]
+    g = synth.make_g("C2", batch=2)
+    out = gu.gpu_solve(cfg.shape, cfg.h, bt["c"], bt["b"], bt["omega"], g)
+    pr, ref = _oracle(cfg.shape, cfg.h, bt["c"], bt["b"], bt["omega"], g, method="lu")
+    for i in range(2):
+        f, bw = ref[i]
+        assert gu.rel(out["z"][i], f["z"]) <= E_Z
+        for k in ("grad_c", "grad_b", "grad_omega"):
+            assert gu.rel(out[k][i], bw[k]) <= E_G, k
+
+
+def test_options_do_not_change_the_answer(gu):
+    """P12: smoother, nu, number of levels change iteration counts, not z*."""
+    from paper_2502_18377_b200 import mpde
+    shape, h = (16, 20, 24), (0.05, 0.05, 0.05)
+    c, b, om, _ = _rand_problem(shape, 2, 41)
+    zs = []
+    for kw in ({}, {"smoother": 0, "nu": 3}, {"levels_max": 2}, {"nu": 1}):
+        out = gu.gpu_solve(shape, h, c, b, om, opts=mpde.mpde_default_options(**kw))
+        zs.append(out["z"])
+    for z in zs[1:]:
+        for i in range(2):
+            assert gu.rel(z[i], zs[0][i]) <= 2 * E_Z
+
+
+def test_nonfinite_input_flagged(gu):
+    shape, h = (12, 12), (0.1, 0.1)
+    c, b, om, _ = _rand_problem(shape, 2, 51)
+    b[1, 7] = np.nan
+    out = gu.gpu_solve(shape, h, c, b, om)
+    assert out["stats_fwd"][0]["status"] == "converged"
+    assert out["stats_fwd"][1]["status"] == "nonfinite"
+
+
+def test_host_abi_matches_device_abi(gu):
+    """mpde_fwd_bwd_host (host buffers, copies inside) == device-pointer path."""
+    from paper_2502_18377_b200 import mpde
+    shape, h = (10, 12, 14), (0.1, 0.08, 0.07)
+    c, b, om, g = _rand_problem(shape, 2, 61)
+    dev = gu.gpu_solve(shape, h, c, b, om, g)
+    prob = mpde.make_problem(shape, h, 2)
+    opts = mpde.mpde_default_options()
+    ws = torch.empty(mpde.mpde_workspace_bytes(prob, opts), dtype=torch.uint8, device="cuda")
+    stg = torch.empty(mpde.mpde_host_staging_bytes(prob), dtype=torch.uint8, device="cuda")
+    t = lambda a: torch.from_numpy(a).pin_memory()
+    z = torch.empty(c.shape, dtype=torch.float32).pin_memory()
+    gc = torch.empty(c.shape, dtype=torch.float32).pin_memory()
+    gb = torch.empty(b.shape, dtype=torch.float32).pin_memory()
+    gw = torch.empty(b.shape, dtype=torch.float32).pin_memory()
+    mpde.mpde_fwd_bwd_host(prob, opts, t(c), t(b), t(om), t(g), z, gc, gb, gw, stg, ws)
+    assert np.array_equal(z.numpy(), dev["z"].astype(np.float32))
+    assert np.array_equal(gc.numpy(), dev["grad_c"].astype(np.float32))
