@@ -174,8 +174,8 @@ def run_ours(a):
     gb = torch.empty((B, P), dtype=torch.float32, device=dev)
     gw = torch.empty_like(gb)
     gsum = torch.empty((M, P), dtype=torch.float32, device=dev)
-    stats_f = torch.zeros((B, 4), dtype=torch.int32, device=dev)
-    stats_b = torch.zeros((B, 4), dtype=torch.int32, device=dev)
+    stats_f = torch.zeros((B, 5), dtype=torch.int32, device=dev)
+    stats_b = torch.zeros((B, 5), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
     def step(i):

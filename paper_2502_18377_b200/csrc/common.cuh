@@ -16,6 +16,7 @@ namespace mpde {
 
 constexpr int kMaxD = 3;
 constexpr int kThreads = 256;
+constexpr int kTabRow = 48;  // floats per (axis, index) row of the condensed-operator tables
 
 // Per-level geometry, passed by value to every kernel.
 struct Geo {
@@ -26,6 +27,11 @@ struct Geo {
   float h[kMaxD], h2[kMaxD];      // h, h^2 (fp32)
   double hd[kMaxD], h2d[kMaxD];   // h, h^2 (fp64)
   float we, wb, wr, ws;           // row-group weights
+  const float* tab;               // device: per-axis row tables of S (schur.cu)
+  int tab_off[kMaxD];             // offset of axis d's rows in tab
+  // interior rows of the tables (identical for 7 <= i <= n-8), kept in the constant bank:
+  // [0,10) Kf o=-2..2 x k, [10,20) KT o=-2..2 x k, [20,29) P0 o=-4..4
+  float irow[kMaxD][32];
 };
 
 // 5-point FD weights for the unit-spaced grid, per class and ascending offset.

@@ -31,7 +31,8 @@ enum {
   SC_REACT = 9,
   SC_LZ_ALPHA = 10,
   SC_LZ_BETA = 11,
-  SC_LZ_EIG = 12
+  SC_LZ_EIG = 12,
+  SC_CORR = 13
 };
 
 struct EpiArgs {
@@ -66,7 +67,10 @@ struct PdeState {
   int* status;
   int* inpass;
   int* failed;
-  float tol;
+  double* dzprev;  // ||delta|| of the previous refinement pass
+  double* errest;  // estimated relative error of z after the last pass
+  float tol;       // residual floor (stop when ||A^T(d-Az)||/||A^T d|| <= tol)
+  float tol_z;     // error-based stop (estimated ||z - z*|| / ||z|| <= tol_z)
 };
 
 int ntiles(int P);
@@ -86,13 +90,17 @@ void launch_ndd_solve(const Geo& G, int B, const float* c, const float* r, float
 void launch_schur_rhs(const Geo& G, int B, const float* c, const float* r, const float* t,
                       float* rt, const int* act, bool f64, cudaStream_t s);
 void launch_backsub(const Geo& G, int B, const float* c, const float* r, const float* dphi,
-                    double* z64, const int* act, bool f64, cudaStream_t s);
+                    double* z64, const int* act, bool f64, double* part, cudaStream_t s);
 // g: per-point scratch, float or double (f64) -- allocate 8 bytes per point
 void launch_schur_g(const Geo& G, int nvec, int crep, const float* c, const float* x, void* g,
                     const int* act, unsigned long long* pts, bool f64, cudaStream_t s);
 void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* c, const float* x,
                       const void* g, const EpiArgs& A, const int* act, bool f64, cudaStream_t s);
-void launch_diag_schur(const Geo& G, int B, const float* c, float* dinv, cudaStream_t s);
+// schur.cu: cf = per-point coefficients [B][2+2D][P] of S (from c), dinv = 1/diag(S)
+void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStream_t s);
+// number of CTAs (= partial sums per vector) of the S kernels on this level
+int schur_tiles(const Geo& G);
+void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaStream_t s);
 void launch_restrict(const Geo& Gf, const Geo& Gc, int nvec, int nfield, const float* fine,
                      float* coarse, const int* act, int crep, cudaStream_t s);
 void launch_prolong(const Geo& Gf, const Geo& Gc, int nvec, const float* coarse, float* fine,

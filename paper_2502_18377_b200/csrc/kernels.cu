@@ -290,303 +290,46 @@ __global__ void __launch_bounds__(kThreads) k_schur_rhs(Geo G, const float* __re
 
 // Back-substitution after the condensed solve:
 //   delta_d = N_dd^-1 (r_d - (N (dphi, 0))_d);  z64 += (dphi, delta_d)
+// Also the per-PDE partials of ||delta||^2 (part) and ||z_new||^2 (part + nvec*tiles) for
+// the error-based refinement stop.
 template <int D, typename T>
 __global__ void __launch_bounds__(kThreads) k_backsub(Geo G, const float* __restrict__ c,
                                                      const float* __restrict__ r,
                                                      const float* __restrict__ dphi,
-                                                     double* __restrict__ z64, const int* act) {
+                                                     double* __restrict__ z64, const int* act,
+                                                     double* part) {
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   if (act && !act[v]) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P) return;
-  int idx[D];
-  unravel<D>(G, p, idx);
-  const float* cb = c + (size_t)v * M * P;
-  const float* xb = dphi + (size_t)v * P;
-  auto zf = [&](int m, int q) -> T { return m == 0 ? T(xb[q]) : T(0); };
-  T out[M];
-  normal_point<D, T, false, true>(G, cb, zf, p, idx, out);
-  T y[M];
-#pragma unroll
-  for (int m = 1; m < M; ++m) y[m] = T(r[((size_t)v * M + m) * P + p]) - out[m];
-  ndd_solve<D, T>(G, cb, p, idx, y);
-  double* zb = z64 + (size_t)v * M * P;
-  zb[p] += double(xb[p]);
-#pragma unroll
-  for (int m = 1; m < M; ++m) zb[m * P + p] += double(y[m]);
-}
-
-// ----------------------------------------------------------------------------------
-// Condensed operator S, pass 1: g(p) (see file header).  x: [nvec][P].
-// ----------------------------------------------------------------------------------
-template <int D, typename T>
-__device__ __forceinline__ T schur_g_point(const Geo& G, const float* __restrict__ cb,
-                                           const float* __restrict__ x, int p, const int* idx) {
-  const int P = G.P;
-  const T xp = x[p];
-  const T wr = G.wr, ws = G.ws, we = G.we;
-  const T wr2 = wr * wr, ws2 = ws * ws;
-  T gv = 0, gu = 0;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const int n = G.n[d], s = G.stride[d], i = idx[d];
-    const T h = geo_h<T>(G, d), h2 = geo_h2<T>(G, d);
-    const int cls = fd_cls(i, n), st = fd_start(cls);
-    T D1 = 0, D2 = 0;
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      const T xv = x[p + (st + q) * s];
-      D1 += fdw<T>(0, cls, q) * xv;
-      D2 += fdw<T>(1, cls, q) * xv;
-    }
-    const bool fw = i <= n - 2, bw = i >= 1;
-    const T sf = fw ? xp - T(x[p + s]) : T(0), sb = bw ? xp - T(x[p - s]) : T(0);
-    const T K1 = -wr2 * h * D1 + ws2 * h * (sf - sb);
-    const T K2 = -wr2 * h2 * D2 + T(0.5) * ws2 * h2 * (sf + sb);
-    T t11, t12, t22;
-    tinv<T>(h, wr, ws, fw, bw, t11, t12, t22);
-    const T v1 = t11 * K1 + t12 * K2, v2 = t12 * K1 + t22 * K2;
-    const T g1 = we * T(cb[(1 + 2 * d) * P + p]), g2 = we * T(cb[(2 + 2 * d) * P + p]);
-    const T u1 = t11 * g1 + t12 * g2, u2 = t12 * g1 + t22 * g2;
-    gv += g1 * v1 + g2 * v2;
-    gu += g1 * u1 + g2 * u2;
-  }
-  return (we * T(cb[p]) * xp - gv) / (T(1) + gu);
-}
-
-template <int D, typename T>
-__global__ void __launch_bounds__(kThreads) k_schur_g(Geo G, const float* __restrict__ c, int crep,
-                                                     const float* __restrict__ x,
-                                                     T* __restrict__ g, const int* act,
-                                                     unsigned long long* pts) {
-  constexpr int M = 1 + 2 * D;
-  const int v = blockIdx.y, P = G.P, pde = v / crep;
-  if (act && !act[pde]) return;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P) return;
-  int idx[D];
-  unravel<D>(G, p, idx);
-  g[(size_t)v * P + p] = schur_g_point<D, T>(G, c + (size_t)pde * M * P, x + (size_t)v * P, p, idx);
-  if (pts && threadIdx.x == 0) atomicAdd(pts, (unsigned long long)min(kThreads, P - p));
-}
-
-// Condensed operator S, pass 2: (S x)(p) = (N zhat)_phi(p), zhat = (x, -w),
-// w_d(p') = T_d^-1 (K_d x)(p') + T_d^-1 gamma_d(p') g(p').
-template <int D, typename T>
-__device__ __forceinline__ T schur_out_point(const Geo& G, const float* __restrict__ cb,
-                                             const float* __restrict__ x,
-                                             const T* __restrict__ g, int p, const int* idx) {
-  const int P = G.P;
-  const T wr = G.wr, ws = G.ws, we = G.we, wr2 = wr * wr, ws2 = ws * ws;
-  const T xp = x[p];
-  T acc = we * T(cb[p]) * g[p];
-  if (on_boundary<D>(G, idx)) acc += T(G.wb) * T(G.wb) * xp;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const int n = G.n[d], s = G.stride[d], i = idx[d];
-    const T h = geo_h<T>(G, d), h2 = geo_h2<T>(G, d);
-    const int lo = max(0, i - 4), hi = min(n - 1, i + 4);
-    for (int ip = lo; ip <= hi; ++ip) {
-      const int di = ip - i;
-      const int cls = fd_cls(ip, n), st = fd_start(cls), j = i - (ip + st);
-      const bool der = (j >= 0) && (j < 5);
-      const bool sm = (di >= -1) && (di <= 1);
-      if (!der && !sm) continue;
-      const int pp = p + di * s;
-      T D1 = 0, D2 = 0;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        const T xv = x[pp + (st + q) * s];
-        D1 += fdw<T>(0, cls, q) * xv;
-        D2 += fdw<T>(1, cls, q) * xv;
-      }
-      const bool fw = ip <= n - 2, bw = ip >= 1;
-      const T xpp = x[pp];
-      const T xn = fw ? T(x[pp + s]) : T(0), xb = bw ? T(x[pp - s]) : T(0);
-      const T sf = fw ? xpp - xn : T(0), sb = bw ? xpp - xb : T(0);
-      const T K1 = -wr2 * h * D1 + ws2 * h * (sf - sb);
-      const T K2 = -wr2 * h2 * D2 + T(0.5) * ws2 * h2 * (sf + sb);
-      T t11, t12, t22;
-      tinv<T>(h, wr, ws, fw, bw, t11, t12, t22);
-      const T g1 = we * T(cb[(1 + 2 * d) * P + pp]), g2 = we * T(cb[(2 + 2 * d) * P + pp]);
-      const T gp = g[pp];
-      const T y1 = K1 + g1 * gp, y2 = K2 + g2 * gp;
-      const T w1 = t11 * y1 + t12 * y2, w2 = t12 * y1 + t22 * y2;
-      if (der) {
-        const T R1 = wr * (-h * w1 - D1), R2 = wr * (-h2 * w2 - D2);
-        acc -= wr * (fdw<T>(0, cls, j) * R1 + fdw<T>(1, cls, j) * R2);
-      }
-      if (sm) {
-        const T sp = fw ? ws * (xpp - h * w1 - T(0.5) * h2 * w2 - xn) : T(0);
-        const T sn = bw ? ws * (xpp + h * w1 - T(0.5) * h2 * w2 - xb) : T(0);
-        if (di == 0)
-          acc += ws * (sp + sn);
-        else if (di == -1)
-          acc -= ws * sp;
-        else
-          acc -= ws * sn;
-      }
-    }
-  }
-  return acc;
-}
-
-// Epilogues fused into the S pass-2 kernel (pointwise vector algebra of PCG and of
-// the polynomial (Jacobi / Chebyshev) smoothers).
-template <int D, int EPI, typename T>
-__global__ void __launch_bounds__(kThreads) k_schur_out(Geo G, const float* __restrict__ c,
-                                                       int crep, const float* __restrict__ x,
-                                                       const T* __restrict__ g, EpiArgs A,
-                                                       const int* act) {
-  constexpr int M = 1 + 2 * D;
-  const int v = blockIdx.y, P = G.P, pde = v / crep;
-  if (act && !act[pde]) return;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  double dot = 0.0;
+  double dd = 0.0, zz = 0.0;
   if (p < P) {
     int idx[D];
     unravel<D>(G, p, idx);
-    const size_t o = (size_t)v * P + p;
-    const float q = float(schur_out_point<D, T>(G, c + (size_t)pde * M * P, x + (size_t)v * P,
-                                                g + (size_t)v * P, p, idx));
-    if (EPI == EPI_STORE) {
-      A.y[o] = q;
-    } else if (EPI == EPI_DOT) {
-      A.y[o] = q;
-      dot = double(x[o]) * q;
-    } else if (EPI == EPI_POWER) {  // Lanczos step: y = D^-1 S x, partial <x, S x>
-      A.y[o] = A.dinv[o] * q;
-      dot = double(x[o]) * q;
-    } else if (EPI == EPI_RESID) {
-      A.res[o] = A.res[o] - q;
-    } else if (EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST) {
-      const float al = A.coef[pde * A.coef_stride + 2 * A.step];
-      const float be = A.coef[pde * A.coef_stride + 2 * A.step + 1];
-      const float res = A.res[o] - q;
-      const float dn = al * x[o] + be * A.dinv[o] * res;
-      const float e = A.e[o] + dn;
-      A.e[o] = e;
-      if (EPI == EPI_SMOOTH) {
-        A.res[o] = res;
-        A.d_out[o] = dn;
-      }
-      if (A.rdot) dot = double(A.rdot[o]) * e;
-    } else if (EPI == EPI_POST0) {
-      const float be = A.coef[pde * A.coef_stride + 1];
-      const float res = A.res[o] - q;
-      const float dn = be * A.dinv[o] * res;
-      const float e = A.e[o] + x[o] + dn;
-      A.e[o] = e;
-      A.res[o] = res;
-      A.d_out[o] = dn;
-      if (A.rdot) dot = double(A.rdot[o]) * e;
+    const float* cb = c + (size_t)v * M * P;
+    const float* xb = dphi + (size_t)v * P;
+    auto zf = [&](int m, int q) -> T { return m == 0 ? T(xb[q]) : T(0); };
+    T out[M];
+    normal_point<D, T, false, true>(G, cb, zf, p, idx, out);
+    T y[M];
+#pragma unroll
+    for (int m = 1; m < M; ++m) y[m] = T(r[((size_t)v * M + m) * P + p]) - out[m];
+    ndd_solve<D, T>(G, cb, p, idx, y);
+    y[0] = T(xb[p]);
+    double* zb = z64 + (size_t)v * M * P;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const double dm = double(y[m]);
+      const double zn = zb[m * P + p] + dm;
+      zb[m * P + p] = zn;
+      dd += dm * dm;
+      zz += zn * zn;
     }
   }
-  if (A.pts && threadIdx.x == 0 && p < P) atomicAdd(A.pts + EPI, (unsigned long long)min(kThreads, P - p));
-  if (EPI == EPI_DOT || EPI == EPI_POWER || ((EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST ||
-                                              EPI == EPI_POST0) && A.rdot)) {
-    dot = block_sum(dot);
-    if (threadIdx.x == 0) A.part[(size_t)v * gridDim.x + blockIdx.x] = dot;
-  }
-}
-
-// ----------------------------------------------------------------------------------
-// 1/diag(S) per point (smoother diagonal).  diag S(p) = N_pp(p,p) -
-// sum_{p'} b(p')^T N_dd(p')^-1 b(p'), b(p') = column p of N_dp restricted to p'.
-// ----------------------------------------------------------------------------------
-template <int D>
-__device__ __forceinline__ void kdphi_coef(int ip, int i, int n, float h, float h2, float wr2,
-                                           float ws2, float& k1, float& k2) {
-  // coefficient of x(i) in (K_d x)_k(ip): der row k at ip + smoothness rows at ip
-  const int cls = fd_cls(ip, n), st = fd_start(cls), j = i - (ip + st);
-  k1 = 0.f;
-  k2 = 0.f;
-  if (j >= 0 && j < 5) {
-    k1 = -wr2 * h * cA[0][cls][j];
-    k2 = -wr2 * h2 * cA[1][cls][j];
-  }
-  const float fw = ip <= n - 2 ? 1.f : 0.f, bw = ip >= 1 ? 1.f : 0.f;
-  const float df = (i == ip ? 1.f : 0.f) - (i == ip + 1 ? 1.f : 0.f);  // sf = x(ip) - x(ip+1)
-  const float db = (i == ip ? 1.f : 0.f) - (i == ip - 1 ? 1.f : 0.f);  // sb = x(ip) - x(ip-1)
-  k1 += ws2 * h * (fw * df - bw * db);
-  k2 += 0.5f * ws2 * h2 * (fw * df + bw * db);
-}
-
-template <int D>
-__global__ void __launch_bounds__(kThreads) k_diag_schur(Geo G, const float* __restrict__ c,
-                                                        float* __restrict__ dinv) {
-  constexpr int M = 1 + 2 * D;
-  const int v = blockIdx.y, P = G.P;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P) return;
-  int idx[D];
-  unravel<D>(G, p, idx);
-  const float* cb = c + (size_t)v * M * P;
-  const float wr2 = G.wr * G.wr, ws2 = G.ws * G.ws;
-  const float cphi = cb[p];
-  double diag = double(G.we) * G.we * cphi * cphi + (on_boundary<D>(G, idx) ? double(G.wb) * G.wb : 0.0);
-  // b at p' = p (all axes) and the own-point Sherman-Morrison terms
-  double bt = 0.0, gt = 0.0, gu = 0.0;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const int n = G.n[d], i = idx[d];
-    const float h = G.h[d], h2 = G.h2[d];
-    // K_pp along axis d at (i,i): der rows touching i + smoothness rows
-    double kpp = 0.0;
-    for (int ip = max(0, i - 4); ip <= min(n - 1, i + 4); ++ip) {
-      const int cls = fd_cls(ip, n), st = fd_start(cls), j = i - (ip + st);
-      if (j >= 0 && j < 5) {
-        kpp += double(wr2) * (double(cA[0][cls][j]) * cA[0][cls][j] + double(cA[1][cls][j]) * cA[1][cls][j]);
-      }
-    }
-    kpp += double(ws2) * (2.0 * (i <= n - 2) + 2.0 * (i >= 1));
-    diag += kpp;
-    float k1, k2;
-    kdphi_coef<D>(i, i, n, h, h2, wr2, ws2, k1, k2);
-    const float g1 = G.we * cb[(1 + 2 * d) * P + p], g2 = G.we * cb[(2 + 2 * d) * P + p];
-    const double b1 = double(k1) + double(g1) * G.we * cphi, b2 = double(k2) + double(g2) * G.we * cphi;
-    double t11, t12, t22;
-    tinv<double>(G.hd[d], G.wr, G.ws, i <= n - 2, i >= 1, t11, t12, t22);
-    const double tb1 = t11 * b1 + t12 * b2, tb2 = t12 * b1 + t22 * b2;
-    bt += b1 * tb1 + b2 * tb2;
-    gt += g1 * tb1 + g2 * tb2;
-    gu += g1 * (t11 * g1 + t12 * g2) + g2 * (t12 * g1 + t22 * g2);
-  }
-  diag -= bt - gt * gt / (1.0 + gu);
-  // neighbours p' = p + di e_d (di != 0): only axis-d slots of b are non-zero
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const int n = G.n[d], s = G.stride[d], i = idx[d];
-    const float h = G.h[d], h2 = G.h2[d];
-    for (int ip = max(0, i - 4); ip <= min(n - 1, i + 4); ++ip) {
-      if (ip == i) continue;
-      float k1, k2;
-      kdphi_coef<D>(ip, i, n, h, h2, wr2, ws2, k1, k2);
-      if (k1 == 0.f && k2 == 0.f) continue;
-      const int pp = p + (ip - i) * s;
-      // sigma(p') needs gamma . T^-1 gamma over all axes at p'
-      double gu2 = 0.0, gtb = 0.0, btb = 0.0;
-      int idx2[D];
-#pragma unroll
-      for (int e = 0; e < D; ++e) idx2[e] = idx[e];
-      idx2[d] = ip;
-#pragma unroll
-      for (int e = 0; e < D; ++e) {
-        double t11, t12, t22;
-        tinv<double>(G.hd[e], G.wr, G.ws, idx2[e] <= G.n[e] - 2, idx2[e] >= 1, t11, t12, t22);
-        const double g1 = double(G.we) * cb[(1 + 2 * e) * P + pp], g2 = double(G.we) * cb[(2 + 2 * e) * P + pp];
-        gu2 += g1 * (t11 * g1 + t12 * g2) + g2 * (t12 * g1 + t22 * g2);
-        if (e == d) {
-          const double tb1 = t11 * k1 + t12 * k2, tb2 = t12 * k1 + t22 * k2;
-          btb = k1 * tb1 + k2 * tb2;
-          gtb = g1 * tb1 + g2 * tb2;
-        }
-      }
-      diag -= btb - gtb * gtb / (1.0 + gu2);
-    }
-  }
-  dinv[(size_t)v * P + p] = float(1.0 / diag);
+  dd = block_sum(dd);
+  if (threadIdx.x == 0) part[(size_t)v * gridDim.x + blockIdx.x] = dd;
+  zz = block_sum(zz);
+  if (threadIdx.x == 0) part[(size_t)gridDim.y * gridDim.x + (size_t)v * gridDim.x + blockIdx.x] = zz;
 }
 
 // ----------------------------------------------------------------------------------
@@ -903,10 +646,18 @@ __device__ __forceinline__ void pcg_fail(const PdeState& st, int v, double val) 
   st.act[v] = 0;
 }
 
+// one warp per PDE: the warp sums the nt CTA partials (lane-strided, then a fixed
+// shuffle tree -- deterministic), lane 0 runs the per-PDE logic.
 __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt, float tol2,
                          int max_iters) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (v >= B) return;
+  double S_ = 0.0;
+  for (int t = lane; t < nt; t += 32) S_ += part[(size_t)v * nt + t];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) S_ += __shfl_xor_sync(0xffffffffu, S_, o);
+  if (lane != 0) return;
+#define sum_parts(a, b, c) S_
   if (op == SC_RHSNORM) {  // ||A^T d||, refinement bookkeeping reset
     st.rhsn[v] = sqrt(sum_parts(part, v, nt));
     st.done[v] = st.rhsn[v] == 0.0 ? 1 : 0;
@@ -915,6 +666,8 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
     st.failed[v] = 0;
     st.status[v] = st.rhsn[v] == 0.0 ? MPDE_STATUS_CONVERGED : MPDE_STATUS_MAXITER;
     st.relres[v] = st.rhsn[v] == 0.0 ? 0.0 : 1.0;
+    st.errest[v] = st.rhsn[v] == 0.0 ? 0.0 : 1.0;
+    st.dzprev[v] = 0.0;
     if (!isfinite(st.rhsn[v])) {
       st.status[v] = MPDE_STATUS_NONFINITE;
       st.done[v] = 1;
@@ -941,16 +694,28 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
     const double rn = sqrt(sum_parts(part, v, nt));
     const double rel = st.rhsn[v] > 0 ? rn / st.rhsn[v] : 0.0;
     st.relres[v] = rel;
-    if (!isfinite(rel)) {
+    if (!isfinite(rel) || !isfinite(st.errest[v])) {
       st.status[v] = MPDE_STATUS_NONFINITE;
       st.done[v] = 1;
-    } else if (rel <= (double)st.tol) {
+    } else if (rel <= (double)st.tol ||
+               (st.refines[v] >= 2 && st.errest[v] <= (double)st.tol_z)) {
       st.status[v] = MPDE_STATUS_CONVERGED;
       st.done[v] = 1;
     } else if (st.failed[v]) {
       st.done[v] = 1;
     }
     st.act[v] = 0;
+    return;
+  }
+  if (op == SC_CORR) {  // after back-substitution: relative error estimate of z
+    if (!st.inpass[v]) return;
+    double S2 = 0.0;  // ||z||^2 partials live in the second half of part
+    for (int t = 0; t < nt; ++t) S2 += part[(size_t)B * nt + (size_t)v * nt + t];
+    const double dz = sqrt(S_), zn = sqrt(S2);
+    // geometric refinement: err_k ~ ||d_k|| * (||d_k|| / ||d_{k-1}||)
+    const double est = st.refines[v] >= 2 && st.dzprev[v] > 0 ? dz * (dz / st.dzprev[v]) : dz;
+    st.dzprev[v] = dz;
+    st.errest[v] = zn > 0 ? est / zn : (dz > 0 ? 1.0 : 0.0);
     return;
   }
   // Lanczos on D^-1 S (self-adjoint in <D.,.>), step index j = max_iters field:
@@ -1033,8 +798,12 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
     st.pass_iters[v] += 1;
     if (!isfinite(rr)) {
       pcg_fail(st, v, rr);
-    } else if (rr <= (double)tol2 * st.rr0[v] || st.pass_iters[v] >= max_iters) {
-      st.act[v] = 0;  // pass finished for this PDE
+    } else if (rr <= (double)tol2 * st.rr0[v] || st.pass_iters[v] >= max_iters ||
+               rr <= 0.25 * (double)st.tol * st.tol * st.rhsn[v] * st.rhsn[v]) {
+      // pass finished: relative inner tolerance (the fp32 limit) reached, or the outer
+      // target itself (after exact back-substitution the full normal residual equals the
+      // condensed one, so the last pass need not over-solve)
+      st.act[v] = 0;
     }
     return;
   }
@@ -1049,6 +818,8 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
     return;
   }
 }
+
+#undef sum_parts
 
 // count of PDEs still active (polled by the host)
 __global__ void k_count_active(int B, const int* act, int* out) {
@@ -1178,6 +949,7 @@ __global__ void k_stats_out(int B, PdeState st, mpde_stats* out) {
   out[v].refines = st.refines[v];
   out[v].status = st.status[v];
   out[v].rel_res = float(st.relres[v]);
+  out[v].err_est = float(st.errest[v]);
 }
 
 // ----------------------------------------------------------------------------------
@@ -1254,46 +1026,12 @@ void launch_schur_rhs(const Geo& G, int B, const float* c, const float* r, const
     DISPATCH_D(G.D, k_schur_rhs<DD, float><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, r, t, rt, act));
 }
 void launch_backsub(const Geo& G, int B, const float* c, const float* r, const float* dphi,
-                    double* z64, const int* act, bool f64, cudaStream_t s) {
+                    double* z64, const int* act, bool f64, double* part, cudaStream_t s) {
   ++g_launch_count;
   if (f64)
-    DISPATCH_D(G.D, k_backsub<DD, double><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, r, dphi, z64, act));
+    DISPATCH_D(G.D, k_backsub<DD, double><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, r, dphi, z64, act, part));
   else
-    DISPATCH_D(G.D, k_backsub<DD, float><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, r, dphi, z64, act));
-}
-void launch_schur_g(const Geo& G, int nvec, int crep, const float* c, const float* x, void* g,
-                    const int* act, unsigned long long* pts, bool f64, cudaStream_t s) {
-  ++g_launch_count;
-  if (f64)
-    DISPATCH_D(G.D, k_schur_g<DD, double><<<grid_for(G.P, nvec), kThreads, 0, s>>>(G, c, crep, x, (double*)g, act, pts));
-  else
-    DISPATCH_D(G.D, k_schur_g<DD, float><<<grid_for(G.P, nvec), kThreads, 0, s>>>(G, c, crep, x, (float*)g, act, pts));
-}
-void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* c, const float* x,
-                      const void* g, const EpiArgs& A, const int* act, bool f64, cudaStream_t s) {
-  ++g_launch_count;
-  dim3 gr = grid_for(G.P, nvec);
-#define EPI_CASE(E)                                                                           \
-  case E:                                                                                     \
-    if (f64)                                                                                  \
-      DISPATCH_D(G.D, k_schur_out<DD, E, double><<<gr, kThreads, 0, s>>>(G, c, crep, x, (const double*)g, A, act)); \
-    else                                                                                      \
-      DISPATCH_D(G.D, k_schur_out<DD, E, float><<<gr, kThreads, 0, s>>>(G, c, crep, x, (const float*)g, A, act)); \
-    break;
-  switch (epi) {
-    EPI_CASE(EPI_STORE)
-    EPI_CASE(EPI_DOT)
-    EPI_CASE(EPI_POWER)
-    EPI_CASE(EPI_RESID)
-    EPI_CASE(EPI_SMOOTH)
-    EPI_CASE(EPI_SMOOTH_LAST)
-    EPI_CASE(EPI_POST0)
-  }
-#undef EPI_CASE
-}
-void launch_diag_schur(const Geo& G, int B, const float* c, float* dinv, cudaStream_t s) {
-  ++g_launch_count;
-  DISPATCH_D(G.D, k_diag_schur<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, dinv));
+    DISPATCH_D(G.D, k_backsub<DD, float><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, r, dphi, z64, act, part));
 }
 void launch_restrict(const Geo& Gf, const Geo& Gc, int nvec, int nfield, const float* fine,
                      float* coarse, const int* act, int crep, cudaStream_t s) {
@@ -1357,7 +1095,7 @@ void launch_coarse_gemv(int n, int nvec, const float* sinv, const float* r, floa
 void launch_scalar(int op, int B, const PdeState& st, const double* part, int nt, float tol2,
                    int max_iters, cudaStream_t s) {
   ++g_launch_count;
-  k_scalar<<<(B + 127) / 128, 128, 0, s>>>(op, B, st, part, nt, tol2, max_iters);
+  k_scalar<<<(B * 32 + 127) / 128, 128, 0, s>>>(op, B, st, part, nt, tol2, max_iters);
 }
 void launch_count_active(int B, const int* act, int* out, cudaStream_t s) {
   ++g_launch_count;

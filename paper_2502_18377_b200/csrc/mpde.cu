@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "internal.h"
@@ -86,7 +88,7 @@ int validate(const mpde_problem* pr, const mpde_options* op) {
     return set_err(MPDE_ERR_INVALID_ARG, "lanczos_steps must be in 2..32");
   if (op->precision < 0 || op->precision > 2)
     return set_err(MPDE_ERR_INVALID_ARG, "precision must be 0, 1 or 2");
-  if (!(op->tol > 0) || !(op->tol_inner > 0))
+  if (!(op->tol > 0) || !(op->tol_inner > 0) || !(op->tol_z > 0))
     return set_err(MPDE_ERR_INVALID_ARG, "tolerances must be > 0");
   return MPDE_OK;
 }
@@ -151,6 +153,101 @@ Geo make_geo(const mpde_problem* pr, const LevelShape& s, int level_scale[kMaxD]
   return G;
 }
 
+// 5-point weights of the k-th derivative row at index i of an n-point axis (P:174,
+// reading Q4): central for 2 <= i <= n-3, one-sided forward/backward at the edges.
+void fd_row(int k, int i, int n, int* off, double* w) {
+  static const double fwd[2][5] = {{-25, 48, -36, 16, -3}, {35, -104, 114, -56, 11}};
+  static const double cen[2][5] = {{1, -8, 0, 8, -1}, {-1, 16, -30, 16, -1}};
+  for (int m = 0; m < 5; ++m) {
+    if (i >= 2 && i <= n - 3) {
+      off[m] = m - 2;
+      w[m] = cen[k][m] / 12.0;
+    } else if (i < 2) {
+      off[m] = m;
+      w[m] = fwd[k][m] / 12.0;
+    } else {
+      off[m] = -m;
+      w[m] = (k == 0 ? -1.0 : 1.0) * fwd[k][m] / 12.0;
+    }
+  }
+}
+
+// Row tables of the condensed operator along one axis (schur.cu header), fp64 -> fp32.
+// Kc[k][i][o]: coefficient of phi(i+o) in the derivative-variable row (k,i) of N
+// (derivative rows, Eq. 5, and Taylor rows, Eqs. 6-7); T_i = N_dd block of axis d;
+// P0 = K_pp - sum_i' Kc(i')^T T_i'^-1 Kc(i').
+void append_axis_tables(int n, double h, double wr, double ws, std::vector<float>& out) {
+  const double wr2 = wr * wr, ws2 = ws * ws;
+  std::vector<double> Kc((size_t)2 * n * 9, 0.0), Ti((size_t)n * 4), A((size_t)2 * n * 9, 0.0);
+  auto kc = [&](int k, int i, int o) -> double& { return Kc[((size_t)k * n + i) * 9 + o + 4]; };
+  auto fa = [&](int k, int i, int o) -> double& { return A[((size_t)k * n + i) * 9 + o + 4]; };
+  for (int i = 0; i < n; ++i) {
+    for (int k = 0; k < 2; ++k) {
+      int off[5];
+      double w[5];
+      fd_row(k, i, n, off, w);
+      const double hk = k == 0 ? h : h * h;
+      for (int m = 0; m < 5; ++m) {
+        fa(k, i, off[m]) += w[m];
+        kc(k, i, off[m]) += -wr2 * hk * w[m];
+      }
+    }
+    const double f = i <= n - 2 ? 1.0 : 0.0, b = i >= 1 ? 1.0 : 0.0;
+    kc(0, i, 0) += ws2 * h * (f - b);
+    kc(1, i, 0) += 0.5 * ws2 * h * h * (f + b);
+    if (f > 0) {
+      kc(0, i, 1) -= ws2 * h;
+      kc(1, i, 1) -= 0.5 * ws2 * h * h;
+    }
+    if (b > 0) {
+      kc(0, i, -1) += ws2 * h;
+      kc(1, i, -1) -= 0.5 * ws2 * h * h;
+    }
+    const double a11 = wr2 * h * h + ws2 * h * h * (f + b), a12 = ws2 * h * h * h * 0.5 * (f - b);
+    const double a22 = wr2 * h * h * h * h + ws2 * h * h * h * h * 0.25 * (f + b);
+    const double det = a11 * a22 - a12 * a12;
+    Ti[i * 4 + 0] = a22 / det;
+    Ti[i * 4 + 1] = -a12 / det;
+    Ti[i * 4 + 2] = -a12 / det;
+    Ti[i * 4 + 3] = a11 / det;
+  }
+  auto kcv = [&](int k, int ip, int j) -> double {  // coefficient of phi(j) in row (k, ip)
+    if (ip < 0 || ip >= n) return 0.0;
+    const int o = j - ip;
+    return (o < -4 || o > 4) ? 0.0 : Kc[((size_t)k * n + ip) * 9 + o + 4];
+  };
+  auto fav = [&](int k, int ip, int j) -> double {
+    const int o = j - ip;
+    return (o < -4 || o > 4) ? 0.0 : A[((size_t)k * n + ip) * 9 + o + 4];
+  };
+  const size_t base = out.size();
+  out.resize(base + (size_t)n * kTabRow, 0.f);
+  for (int i = 0; i < n; ++i) {
+    float* row = out.data() + base + (size_t)i * kTabRow;
+    for (int o = -4; o <= 4; ++o)
+      for (int k = 0; k < 2; ++k) {
+        row[(o + 4) * 2 + k] = float(kcv(k, i, i + o));         // Kf
+        row[18 + (o + 4) * 2 + k] = float(kcv(k, i + o, i));    // KT
+      }
+    for (int o = -5; o <= 5; ++o) {
+      const int j = i + o;
+      if (j < 0 || j >= n) continue;
+      double v = 0.0;
+      for (int ip = std::max(0, std::max(i, j) - 4); ip <= std::min(n - 1, std::min(i, j) + 4); ++ip) {
+        for (int k = 0; k < 2; ++k) v += wr2 * fav(k, ip, i) * fav(k, ip, j);  // K_pp der rows
+        for (int k = 0; k < 2; ++k)
+          for (int l = 0; l < 2; ++l) v -= kcv(k, ip, i) * Ti[ip * 4 + k * 2 + l] * kcv(l, ip, j);
+      }
+      // K_pp Taylor rows: forward rows (e_i' - e_i'+1), backward rows (e_i' - e_i'-1)
+      for (int ip = std::max(0, std::min(i, j) - 1); ip <= std::min(n - 1, std::max(i, j) + 1); ++ip) {
+        if (ip <= n - 2) v += ws2 * ((i == ip) - (i == ip + 1)) * ((j == ip) - (j == ip + 1));
+        if (ip >= 1) v += ws2 * ((i == ip) - (i == ip - 1)) * ((j == ip) - (j == ip - 1));
+      }
+      row[36 + o + 5] = float(v);
+    }
+  }
+}
+
 struct Bump {
   char* base;
   size_t off = 0;
@@ -207,6 +304,9 @@ struct Level {
   double* lmax;     // [B]
   float* coef;      // [B][2 nu]
   float *r, *e, *d, *d2, *g, *pe;  // [B][P]
+  float* cf;        // [B][2+2D][P] per-point coefficients of S (schur.cu)
+  float* tab;       // device row tables of S, sum_d n_d * kTabRow floats
+  std::vector<float> tab_host;
 };
 
 struct mpde_hierarchy {
@@ -226,8 +326,10 @@ struct mpde_hierarchy {
   double* part;
   int part_nt;
   PdeState st;
-  int* d_count;
-  int* h_count;  // pinned
+  int* d_count;  // [2]
+  int* h_count;  // pinned [2]
+  cudaEvent_t ev[2];
+  char* ws_base;
   int* ones;     // [B] all 1
   float* rho;    // [B][P] equation residual b - c.z* of the last forward (fp64-derived)
   const float* rho_b;  // rhs_b it was computed for
@@ -257,6 +359,16 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
     lv.G = make_geo(pr, shp[l], scale);
     lv.P = shp[l].P;
     lv.cbuf = l > 0 ? bp.take<float>((size_t)B * M * lv.P) : nullptr;
+    lv.cf = bp.take<float>((size_t)B * (2 + 2 * D) * lv.P);
+    {
+      int off = 0;
+      for (int d = 0; d < D; ++d) {
+        lv.G.tab_off[d] = off;
+        off += shp[l].n[d] * kTabRow;
+      }
+      lv.tab = bp.take<float>((size_t)off);
+      lv.G.tab = lv.tab;
+    }
     lv.dinv = bp.take<float>((size_t)B * lv.P);
     lv.lmax = bp.take<double>(B);
     lv.coef = bp.take<float>((size_t)B * 2 * op->nu);
@@ -273,7 +385,7 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
   h->p = bp.take<float>((size_t)B * P);
   h->q = bp.take<float>((size_t)B * P);
   h->part_nt = ntiles(P);
-  h->part = bp.take<double>((size_t)B * h->part_nt + 64);
+  h->part = bp.take<double>((size_t)2 * B * h->part_nt + 64);  // 2 slots (backsub)
   h->st.rz = bp.take<double>(B);
   h->st.rr0 = bp.take<double>(B);
   h->st.rhsn = bp.take<double>(B);
@@ -291,7 +403,9 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
   h->rho = bp.take<float>((size_t)B * P);
   h->st.inpass = bp.take<int>(B);
   h->st.failed = bp.take<int>(B);
-  h->d_count = bp.take<int>(1);
+  h->st.dzprev = bp.take<double>(B);
+  h->st.errest = bp.take<double>(B);
+  h->d_count = bp.take<int>(2);
   h->ones = bp.take<int>(B);
   // union: full-system solve vectors | coarsest probing scratch
   const size_t u0 = bp.off;
@@ -333,9 +447,9 @@ int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const flo
   Level& lv = h->lv[l];
   EpiArgs A2 = A;
   A2.pts = g_prof.on ? g_prof.d_pts : nullptr;
-  PROF(0, s, launch_schur_g(lv.G, nvec, crep, lv.c, x, lv.g, act, A2.pts ? A2.pts + 8 : nullptr,
+  PROF(0, s, launch_schur_g(lv.G, nvec, crep, lv.cf, x, lv.g, act, A2.pts ? A2.pts + 8 : nullptr,
                             f64, s));
-  PROF(1, s, launch_schur_out(epi, lv.G, nvec, crep, lv.c, x, lv.g, A2, act, f64, s));
+  PROF(1, s, launch_schur_out(epi, lv.G, nvec, crep, lv.cf, x, lv.g, A2, act, f64, s));
   CKL();
   return MPDE_OK;
 }
@@ -407,6 +521,51 @@ int poll_active(mpde_hierarchy* h, cudaStream_t s, int* nact) {
   return MPDE_OK;
 }
 
+// CUDA graph of `k` PCG iterations, cached per (workspace base, problem, options): a
+// hierarchy rebuilt in the same workspace for the same problem has identical device
+// pointers and kernel parameters, so the instantiated graph stays valid across builds.
+// Captured on a private stream (the legacy default stream cannot be captured); the
+// graph is launched on the caller's stream.
+std::mutex g_graph_mu;
+std::map<std::string, std::pair<cudaGraphExec_t, unsigned long long>> g_graphs;
+cudaStream_t g_capture_stream = nullptr;
+
+template <class F>
+int chunk_graph(mpde_hierarchy* h, int k, F& iteration, cudaGraphExec_t* out,
+                unsigned long long* nodes) {
+  std::string key((const char*)&h->ws_base, sizeof(h->ws_base));
+  key.append((const char*)&h->prob, sizeof(h->prob));
+  key.append((const char*)&h->opts, sizeof(h->opts));
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  auto it = g_graphs.find(key);
+  if (it != g_graphs.end()) {
+    *out = it->second.first;
+    *nodes = it->second.second;
+    return MPDE_OK;
+  }
+  if (!g_capture_stream) CK(cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking));
+  cudaGraph_t graph = nullptr;
+  const unsigned long long l0 = g_launch_count;
+  CK(cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = MPDE_OK;
+  for (int i = 0; i < k && rc == MPDE_OK; ++i) rc = iteration(g_capture_stream);
+  const cudaError_t e = cudaStreamEndCapture(g_capture_stream, &graph);
+  const unsigned long long n = g_launch_count - l0;
+  g_launch_count = l0;  // captured, not launched: counted at every replay instead
+  if (rc) return rc;
+  if (e != cudaSuccess)
+    return set_err(MPDE_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e2 = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e2 != cudaSuccess)
+    return set_err(MPDE_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2));
+  g_graphs[key] = {exec, n};
+  *out = exec;
+  *nodes = n;
+  return MPDE_OK;
+}
+
 // k_dot partial for rr0: reuse pcg_update with alpha = 0 would touch p; use a dedicated path
 __global__ void k_dot_self(int P, const float* __restrict__ r, double* part, const int* act) {
   const int v = blockIdx.y;
@@ -424,8 +583,9 @@ __global__ void k_dot_self(int P, const float* __restrict__ r, double* part, con
 // PCG on the condensed system S x = rp (level 0), x0 = 0.
 int pcg(mpde_hierarchy* h, cudaStream_t s) {
   const int B = h->B, P = h->P;
-  const int nt = ntiles(P);
-  const int ntc = h->L == 1 ? coarse_gemv_blocks(h->Pc) : nt;
+  const int nt = ntiles(P);                  // partials of the pointwise vector kernels
+  const int nts = schur_tiles(h->lv[0].G);   // partials of the S kernels
+  const int ntc = h->L == 1 ? coarse_gemv_blocks(h->Pc) : nts;
   const float tol2 = h->opts.tol_inner * h->opts.tol_inner;
   const int* act = h->st.act;
   Level& l0 = h->lv[0];
@@ -438,24 +598,46 @@ int pcg(mpde_hierarchy* h, cudaStream_t s) {
   PROF(7, s, launch_scalar(SC_RZ0, B, h->st, h->part, ntc, tol2, h->opts.max_iters, s));
   PROF(6, s, launch_p_update(P, B, h->st.beta, l0.e, h->p, act, s));
   CKL();
-  for (int it = 0; it < h->opts.max_iters; ++it) {
+  // one PCG iteration (P:255 Krylov step with the V-cycle of P:262-275); every PDE that
+  // has converged or failed is masked on the device, so extra iterations are no-ops
+  auto iteration = [&](cudaStream_t st) -> int {
     EpiArgs A;
     A.y = h->q;
     A.part = h->part;
-    if (int rc = schur_apply(h, 0, EPI_DOT, B, 1, h->p, A, act, f64_outer(h), s)) return rc;
-    PROF(7, s, launch_scalar(SC_ALPHA, B, h->st, h->part, nt, tol2, h->opts.max_iters, s));
-    PROF(6, s, launch_pcg_update(P, B, h->st.alpha, h->p, h->q, h->x, h->rp, h->part, act, s));
-    PROF(7, s, launch_scalar(SC_CONV, B, h->st, h->part, nt, tol2, h->opts.max_iters, s));
+    if (int rc = schur_apply(h, 0, EPI_DOT, B, 1, h->p, A, act, f64_outer(h), st)) return rc;
+    PROF(7, st, launch_scalar(SC_ALPHA, B, h->st, h->part, nts, tol2, h->opts.max_iters, st));
+    PROF(6, st, launch_pcg_update(P, B, h->st.alpha, h->p, h->q, h->x, h->rp, h->part, act, st));
+    PROF(7, st, launch_scalar(SC_CONV, B, h->st, h->part, nt, tol2, h->opts.max_iters, st));
+    if (int rc = vcycle(h, 0, h->rp, h->rp, h->part, act, st)) return rc;
+    PROF(7, st, launch_scalar(SC_BETA, B, h->st, h->part, ntc, tol2, h->opts.max_iters, st));
+    PROF(6, st, launch_p_update(P, B, h->st.beta, l0.e, h->p, act, st));
     CKL();
-    if ((it + 1) % h->opts.poll_every == 0 || it + 1 == h->opts.max_iters) {
-      int nact = 0;
-      if (int rc = poll_active(h, s, &nact)) return rc;
-      if (nact == 0) break;
+    return MPDE_OK;
+  };
+  const int k = h->opts.poll_every;
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long nodes = 0;
+  if (!g_prof.on && h->opts.use_graphs) {
+    if (int rc = chunk_graph(h, k, iteration, &exec, &nodes)) return rc;
+  }
+  // pipelined polling: chunk j+1 is enqueued before chunk j's active count is read
+  const int nchunks = (h->opts.max_iters + k - 1) / k;
+  for (int j = 0; j < nchunks; ++j) {
+    if (exec) {
+      CK(cudaGraphLaunch(exec, s));
+      g_launch_count += nodes;
+    } else {
+      for (int i = 0; i < k; ++i)
+        if (int rc = iteration(s)) return rc;
     }
-    if (int rc = vcycle(h, 0, h->rp, h->rp, h->part, act, s)) return rc;
-    PROF(7, s, launch_scalar(SC_BETA, B, h->st, h->part, ntc, tol2, h->opts.max_iters, s));
-    PROF(6, s, launch_p_update(P, B, h->st.beta, l0.e, h->p, act, s));
-    CKL();
+    PROF(7, s, launch_count_active(B, h->st.act, h->d_count + (j & 1), s));
+    CK(cudaMemcpyAsync(h->h_count + (j & 1), h->d_count + (j & 1), sizeof(int),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(h->ev[j & 1], s));
+    if (j >= 1) {
+      CK(cudaEventSynchronize(h->ev[(j - 1) & 1]));
+      if (h->h_count[(j - 1) & 1] == 0) break;
+    }
   }
   return MPDE_OK;
 }
@@ -482,7 +664,9 @@ int solve_core(mpde_hierarchy* h, const float* rhs, const float* b, const float*
     if (int rc = pcg(h, s)) return rc;
     // re-activate every PDE still being refined (PCG deactivated converged ones)
     PROF(7, s, launch_scalar(SC_REACT, B, h->st, h->part, nt, 0.f, 0, s));
-    PROF(4, s, launch_backsub(l0.G, B, l0.c, h->rfull, h->x, h->z64, h->st.act, f64_outer(h), s));
+    PROF(4, s, launch_backsub(l0.G, B, l0.c, h->rfull, h->x, h->z64, h->st.act, f64_outer(h),
+                              h->part, s));
+    PROF(7, s, launch_scalar(SC_CORR, B, h->st, h->part, nt, 0.f, 0, s));
     PROF(2, s, launch_residual64(l0.G, B, l0.c, rhs, b, om, h->z64, h->rfull, h->part, h->st.act, s));
     PROF(7, s, launch_scalar(SC_REFRES, B, h->st, h->part, nt, 0.f, 0, s));
     CKL();
@@ -499,8 +683,9 @@ extern "C" {
 
 mpde_options mpde_default_options(void) {
   mpde_options o;
-  o.tol = 1e-7f;
-  o.tol_inner = 1e-4f;
+  o.tol = 1e-10f;
+  o.tol_z = 1e-4f;
+  o.tol_inner = 3e-4f;
   o.max_iters = 500;
   o.max_refine = 6;
   o.smoother = 1;
@@ -512,6 +697,7 @@ mpde_options mpde_default_options(void) {
   o.cheb_ratio = 30.f;
   o.lanczos_steps = 16;
   o.precision = 1;
+  o.use_graphs = 1;
   return o;
 }
 
@@ -556,17 +742,21 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
   h->prob = *prob;
   h->opts = *opts;
   plan_workspace(prob, opts, (char*)workspace, h);
+  h->ws_base = (char*)workspace;
   if (h->Pc > kMaxCoarse) {
     delete h;
     return set_err(MPDE_ERR_UNSUPPORTED,
                    "coarsest level has %d points (> %d); raise levels_max / lower coarsest",
                    h->Pc, kMaxCoarse);
   }
-  if (cudaHostAlloc(&h->h_count, sizeof(int), cudaHostAllocDefault) != cudaSuccess) {
+  if (cudaHostAlloc(&h->h_count, 2 * sizeof(int), cudaHostAllocDefault) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev[1], cudaEventDisableTiming) != cudaSuccess) {
     delete h;
     return set_err(MPDE_ERR_CUDA, "cudaHostAlloc failed");
   }
   h->st.tol = opts->tol;
+  h->st.tol_z = opts->tol_z;
   const int B = h->B, M = h->M, L = h->L;
   g_launch_count += 2;
   k_fill_int<<<(B + 255) / 256, 256, 0, s>>>(B, h->ones, 1);
@@ -581,7 +771,25 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
   CKL();
   for (int l = 0; l < L; ++l) {
     Level& lv = h->lv[l];
-    launch_diag_schur(lv.G, B, lv.c, lv.dinv, s);
+    // per-axis row tables of S (host, fp64 -> fp32) and per-point coefficients
+    lv.tab_host.clear();
+    for (int d = 0; d < h->prob.ndim; ++d)
+      append_axis_tables(lv.G.n[d], lv.G.hd[d], lv.G.wr, lv.G.ws, lv.tab_host);
+    CK(cudaMemcpyAsync(lv.tab, lv.tab_host.data(), sizeof(float) * lv.tab_host.size(),
+                       cudaMemcpyHostToDevice, s));
+    for (int d = 0; d < h->prob.ndim; ++d) {  // interior rows -> kernel params
+      // Kf rows are identical for 2 <= i <= n-3; KT and P0 rows for 7 <= i <= n-8 (n >= 15)
+      const int n = lv.G.n[d];
+      const float* row = lv.tab_host.data() + lv.G.tab_off[d] + (size_t)(n / 2) * kTabRow;
+      for (int o = -2; o <= 2; ++o)
+        for (int k = 0; k < 2; ++k) {
+          lv.G.irow[d][(o + 2) * 2 + k] = row[(o + 4) * 2 + k];
+          lv.G.irow[d][10 + (o + 2) * 2 + k] = n >= 15 ? row[18 + (o + 4) * 2 + k] : 0.f;
+        }
+      for (int o = -4; o <= 4; ++o) lv.G.irow[d][20 + o + 4] = n >= 15 ? row[36 + o + 5] : 0.f;
+    }
+    launch_schur_coef(lv.G, B, lv.c, lv.cf, s);
+    launch_diag_schur(lv.G, B, lv.cf, lv.dinv, s);
     CKL();
     if (l == L - 1) break;
     // lambda_max(D^-1 S) per PDE: Lanczos in the D-inner product (D = diag S), then the
@@ -606,7 +814,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
         delete h;
         return rc;
       }
-      launch_scalar(SC_LZ_ALPHA, B, sl, h->part, nt, 0.f, j, s);
+      launch_scalar(SC_LZ_ALPHA, B, sl, h->part, schur_tiles(lv.G), 0.f, j, s);
       launch_lz_update(lv.P, B, y, v, vp, lv.dinv, h->st.alpha, h->st.beta, h->part, s);
       launch_scalar(SC_LZ_BETA, B, sl, h->part, nt, 0.f, j, s);
       launch_scale(lv.P, B, h->st.alpha, vp, vp, h->ones, s);
@@ -626,7 +834,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
     for (int b0 = 0; b0 < B; b0 += chunk) {
       const int nb = std::min(chunk, B - b0);
       const size_t vo = (size_t)b0 * Pc * Pc;
-      const float* cc = lc.c + (size_t)b0 * M * Pc;
+      const float* cc = lc.cf + (size_t)b0 * (M + 1) * Pc;  // cf has 2+2D = M+1 fields
       launch_identity(Pc, nb * Pc, h->probe_x + vo, s);
       launch_schur_g(lc.G, nb * Pc, Pc, cc, h->probe_x + vo, h->probe_g + 2 * vo, nullptr, nullptr,
                      f64_outer(h), s);
@@ -645,6 +853,8 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
 int mpde_destroy_hierarchy(mpde_hierarchy* h) {
   if (!h) return MPDE_OK;
   if (h->h_count) cudaFreeHost(h->h_count);
+  if (h->ev[0]) cudaEventDestroy(h->ev[0]);
+  if (h->ev[1]) cudaEventDestroy(h->ev[1]);
   delete h;
   return MPDE_OK;
 }

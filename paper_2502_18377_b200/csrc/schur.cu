@@ -1,0 +1,665 @@
+// schur.cu -- the condensed normal operator S (Schur complement of A^T A onto u_phi).
+//
+// Exact algebra: with per-point alpha = w_eq c_phi, gamma_d = w_eq c_d,
+// u_d = T_d^-1 gamma_d, sigma = 1/(1 + sum_d gamma_d . u_d) and the per-axis 1D operators
+//   K_d   : the derivative-variable rows of N applied to phi (der + Taylor rows, Eqs. 5-7)
+//   P0_d  = K_pp,d - K_d^T T_d^-1 K_d      (Schur complement of the constant part)
+// the operator is
+//   h(p)  = (1/sigma) * ( sigma alpha x - sum_d u~_d . (K_d x)(p) ),   u~ = sigma u
+//   S x   = sum_d P0_d x - sum_d K_d^T (u~_d h) + sigma alpha h + w_bnd^2 [p in B] x.
+// K_d, K_d^T and P0_d depend only on the index along axis d (13 classes near the edges,
+// constant inside): their rows are tabulated on the host in fp64 (no run-time
+// cancellation of the large h^-k terms) -- 48 floats per (axis, index):
+//   [0,18)  Kf[o][k]  coefficient of x(i+o) in (K x)_k(i),      o = -4..4
+//   [18,36) KT[o][k]  coefficient of q_k(i+o) in (K^T q)(i),    o = -4..4
+//   [36,47) P0[o]     coefficient of x(i+o) in (P0 x)(i),       o = -5..5
+// Per point the kernels read cf = [sigma alpha, 1/sigma, u~ (2D)] (2+2D floats).
+#include "common.cuh"
+#include "internal.h"
+
+namespace mpde {
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_schur_coef(Geo G, const float* __restrict__ c,
+                                                        float* __restrict__ cf) {
+  constexpr int M = 1 + 2 * D, NC = 2 + 2 * D;
+  const int v = blockIdx.y, P = G.P;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int idx[D];
+  unravel<D>(G, p, idx);
+  const float* cb = c + (size_t)v * M * P;
+  float* out = cf + (size_t)v * NC * P;
+  const double we = G.we;
+  double u[2 * D];
+  double s = 1.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    double t11, t12, t22;
+    tinv<double>(G.hd[d], G.wr, G.ws, idx[d] <= G.n[d] - 2, idx[d] >= 1, t11, t12, t22);
+    const double g1 = we * cb[(1 + 2 * d) * P + p], g2 = we * cb[(2 + 2 * d) * P + p];
+    u[2 * d] = t11 * g1 + t12 * g2;
+    u[2 * d + 1] = t12 * g1 + t22 * g2;
+    s += g1 * u[2 * d] + g2 * u[2 * d + 1];
+  }
+  const double sig = 1.0 / s;
+  out[p] = float(sig * we * cb[p]);
+  out[P + p] = float(s);
+#pragma unroll
+  for (int q = 0; q < 2 * D; ++q) out[(size_t)(2 + q) * P + p] = float(sig * u[q]);
+}
+
+__device__ __forceinline__ const float* tab_row(const Geo& G, int d, int i) {
+  return G.tab + G.tab_off[d] + i * kTabRow;
+}
+
+// pass 1: h(p)
+template <int D, typename T>
+__device__ __forceinline__ T schur_h_point(const Geo& G, const float* __restrict__ cf,
+                                           const float* __restrict__ x, int p, const int* idx) {
+  const int P = G.P;
+  T g = T(cf[p]) * T(x[p]);
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const int n = G.n[d], s = G.stride[d], i = idx[d];
+    const float* row = tab_row(G, d, i);
+    T k1 = 0, k2 = 0;
+    if (i >= 2 && i <= n - 3) {
+#pragma unroll
+      for (int o = -2; o <= 2; ++o) {
+        const T xv = x[p + o * s];
+        k1 += T(__ldg(row + (o + 4) * 2)) * xv;
+        k2 += T(__ldg(row + (o + 4) * 2 + 1)) * xv;
+      }
+    } else {
+      const int lo = max(-4, -i), hi = min(4, n - 1 - i);
+      for (int o = lo; o <= hi; ++o) {
+        const T xv = x[p + o * s];
+        k1 += T(__ldg(row + (o + 4) * 2)) * xv;
+        k2 += T(__ldg(row + (o + 4) * 2 + 1)) * xv;
+      }
+    }
+    g -= T(cf[(size_t)(2 + 2 * d) * P + p]) * k1 + T(cf[(size_t)(3 + 2 * d) * P + p]) * k2;
+  }
+  return T(cf[P + p]) * g;
+}
+
+// pass 2: (S x)(p)
+template <int D, typename T>
+__device__ __forceinline__ T schur_s_point(const Geo& G, const float* __restrict__ cf,
+                                           const float* __restrict__ x, const T* __restrict__ hb,
+                                           int p, const int* idx) {
+  const int P = G.P;
+  T acc = T(cf[p]) * hb[p];
+  if (on_boundary<D>(G, idx)) acc += T(G.wb) * T(G.wb) * T(x[p]);
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const int n = G.n[d], s = G.stride[d], i = idx[d];
+    const float* row = tab_row(G, d, i);
+    const float* u1 = cf + (size_t)(2 + 2 * d) * P;
+    const float* u2 = cf + (size_t)(3 + 2 * d) * P;
+    if (i >= 7 && i <= n - 8) {  // P0 reach 4 and K^T reach 2 away from the edge classes
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) acc += T(__ldg(row + 36 + o + 5)) * T(x[p + o * s]);
+#pragma unroll
+      for (int o = -2; o <= 2; ++o) {
+        const int q = p + o * s;
+        acc -= (T(__ldg(row + 18 + (o + 4) * 2)) * T(u1[q]) +
+                T(__ldg(row + 18 + (o + 4) * 2 + 1)) * T(u2[q])) * hb[q];
+      }
+    } else {
+      const int lo = max(-5, -i), hi = min(5, n - 1 - i);
+      for (int o = lo; o <= hi; ++o) acc += T(__ldg(row + 36 + o + 5)) * T(x[p + o * s]);
+      const int lo2 = max(-4, -i), hi2 = min(4, n - 1 - i);
+      for (int o = lo2; o <= hi2; ++o) {
+        const int q = p + o * s;
+        acc -= (T(__ldg(row + 18 + (o + 4) * 2)) * T(u1[q]) +
+                T(__ldg(row + 18 + (o + 4) * 2 + 1)) * T(u2[q])) * hb[q];
+      }
+    }
+  }
+  return acc;
+}
+
+template <int D, typename T>
+__global__ void __launch_bounds__(kThreads) k_schur_h(Geo G, const float* __restrict__ cf, int crep,
+                                                     const float* __restrict__ x,
+                                                     T* __restrict__ hout, const int* act,
+                                                     unsigned long long* pts) {
+  constexpr int NC = 2 + 2 * D;
+  const int v = blockIdx.y, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int idx[D];
+  unravel<D>(G, p, idx);
+  hout[(size_t)v * P + p] =
+      schur_h_point<D, T>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, p, idx);
+  if (pts && threadIdx.x == 0) atomicAdd(pts, (unsigned long long)min(kThreads, P - p));
+}
+
+// pass 2 with the fused PCG / smoother epilogues (same contract as EpiArgs in internal.h)
+template <int D, int EPI, typename T>
+__global__ void __launch_bounds__(kThreads) k_schur_s(Geo G, const float* __restrict__ cf, int crep,
+                                                     const float* __restrict__ x,
+                                                     const T* __restrict__ hb, EpiArgs A,
+                                                     const int* act) {
+  constexpr int NC = 2 + 2 * D;
+  const int v = blockIdx.y, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  double dot = 0.0;
+  if (p < P) {
+    int idx[D];
+    unravel<D>(G, p, idx);
+    const size_t o = (size_t)v * P + p;
+    const float q = float(schur_s_point<D, T>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P,
+                                              hb + (size_t)v * P, p, idx));
+    if (EPI == EPI_STORE) {
+      A.y[o] = q;
+    } else if (EPI == EPI_DOT) {
+      A.y[o] = q;
+      dot = double(x[o]) * q;
+    } else if (EPI == EPI_POWER) {  // Lanczos step: y = D^-1 S x, partial <x, S x>
+      A.y[o] = A.dinv[o] * q;
+      dot = double(x[o]) * q;
+    } else if (EPI == EPI_RESID) {
+      A.res[o] = A.res[o] - q;
+    } else if (EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST) {
+      const float al = A.coef[pde * A.coef_stride + 2 * A.step];
+      const float be = A.coef[pde * A.coef_stride + 2 * A.step + 1];
+      const float res = A.res[o] - q;
+      const float dn = al * x[o] + be * A.dinv[o] * res;
+      const float e = A.e[o] + dn;
+      A.e[o] = e;
+      if (EPI == EPI_SMOOTH) {
+        A.res[o] = res;
+        A.d_out[o] = dn;
+      }
+      if (A.rdot) dot = double(A.rdot[o]) * e;
+    } else if (EPI == EPI_POST0) {
+      const float be = A.coef[pde * A.coef_stride + 1];
+      const float res = A.res[o] - q;
+      const float dn = be * A.dinv[o] * res;
+      const float e = A.e[o] + x[o] + dn;
+      A.e[o] = e;
+      A.res[o] = res;
+      A.d_out[o] = dn;
+      if (A.rdot) dot = double(A.rdot[o]) * e;
+    }
+  }
+  if (A.pts && threadIdx.x == 0 && p < P)
+    atomicAdd(A.pts + EPI, (unsigned long long)min(kThreads, P - p));
+  if (EPI == EPI_DOT || EPI == EPI_POWER ||
+      ((EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST || EPI == EPI_POST0) && A.rdot)) {
+    dot = block_sum(dot);
+    if (threadIdx.x == 0) A.part[(size_t)v * gridDim.x + blockIdx.x] = dot;
+  }
+}
+
+// 1/diag(S) (smoother diagonal), fp64: diag = sum_d P0_d(i,i) + w_bnd^2 [B]
+//   + (sigma alpha) dh(p)/dx(p) - sum_d sum_o sum_k KT[o][k] u~_dk(q) dh(q)/dx(p), q = p + o e_d
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_schur_diag(Geo G, const float* __restrict__ cf,
+                                                        float* __restrict__ dinv) {
+  constexpr int NC = 2 + 2 * D;
+  const int v = blockIdx.y, P = G.P;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int idx[D];
+  unravel<D>(G, p, idx);
+  const float* cb = cf + (size_t)v * NC * P;
+  double dhp = cb[p];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const float* row = tab_row(G, d, idx[d]);
+    dhp -= double(cb[(size_t)(2 + 2 * d) * P + p]) * row[8] + double(cb[(size_t)(3 + 2 * d) * P + p]) * row[9];
+  }
+  dhp *= double(cb[P + p]);
+  double diag = double(cb[p]) * dhp + (on_boundary<D>(G, idx) ? double(G.wb) * G.wb : 0.0);
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const int n = G.n[d], s = G.stride[d], i = idx[d];
+    const float* row = tab_row(G, d, i);
+    diag += row[36 + 5];
+    for (int o = max(-4, -i); o <= min(4, n - 1 - i); ++o) {
+      const int q = p + o * s;
+      double dh;
+      if (o == 0) {
+        dh = dhp;
+      } else {
+        const float* rq = tab_row(G, d, i + o);  // coefficient of x(i) in (K x)(i+o)
+        dh = -double(cb[(size_t)(2 + 2 * d) * P + q]) * rq[(-o + 4) * 2] -
+             double(cb[(size_t)(3 + 2 * d) * P + q]) * rq[(-o + 4) * 2 + 1];
+        dh *= double(cb[P + q]);
+      }
+      diag -= (double(row[18 + (o + 4) * 2]) * cb[(size_t)(2 + 2 * d) * P + q] +
+               double(row[18 + (o + 4) * 2 + 1]) * cb[(size_t)(3 + 2 * d) * P + q]) * dh;
+    }
+  }
+  dinv[(size_t)v * P + p] = float(1.0 / diag);
+}
+
+// ---------------------------------------------------------------------------------
+// Vectorised variants: 4 consecutive points along the contiguous (last) axis per thread
+// (requires n_last % 4 == 0).  Non-last axes: one float4 load per stencil offset serves
+// the 4 points; last axis: a register window loaded with aligned float4s.  Interior rows
+// of the tables come from the constant bank (G.irow); edge rows from the global table.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+template <typename T>
+__device__ __forceinline__ void ldT4(const T* p, T* v) {
+  if (sizeof(T) == 4) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  } else {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void stT4(T* p, const T* v) {
+  if (sizeof(T) == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(float(v[0]), float(v[1]), float(v[2]), float(v[3]));
+  } else {
+    *reinterpret_cast<double2*>(p) = make_double2(double(v[0]), double(v[1]));
+    *reinterpret_cast<double2*>(p + 2) = make_double2(double(v[2]), double(v[3]));
+  }
+}
+#define F4(a, j) (j == 0 ? a.x : (j == 1 ? a.y : (j == 2 ? a.z : a.w)))
+
+template <int D, typename T>
+__device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__ cb,
+                                         const float* __restrict__ xb, int p0, const int* idx,
+                                         T* g) {
+  const int P = G.P;
+  {
+    const float4 x0 = ld4(xb + p0), c0 = ld4(cb + p0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g[j] = T(F4(c0, j)) * T(F4(x0, j));
+  }
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) {
+    const int n = G.n[d], s = G.stride[d], i = idx[d];
+    T k1[4] = {0, 0, 0, 0}, k2[4] = {0, 0, 0, 0};
+    if (i >= 2 && i <= n - 3) {
+#pragma unroll
+      for (int o = -2; o <= 2; ++o) {
+        const float4 xv = ld4(xb + p0 + o * s);
+        const T a = G.irow[d][(o + 2) * 2], b = G.irow[d][(o + 2) * 2 + 1];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          k1[j] += a * T(F4(xv, j));
+          k2[j] += b * T(F4(xv, j));
+        }
+      }
+    } else {
+      const float* row = tab_row(G, d, i);
+      for (int o = max(-4, -i); o <= min(4, n - 1 - i); ++o) {
+        const float4 xv = ld4(xb + p0 + o * s);
+        const T a = __ldg(row + (o + 4) * 2), b = __ldg(row + (o + 4) * 2 + 1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          k1[j] += a * T(F4(xv, j));
+          k2[j] += b * T(F4(xv, j));
+        }
+      }
+    }
+    const float4 ua = ld4(cb + (size_t)(2 + 2 * d) * P + p0), ub = ld4(cb + (size_t)(3 + 2 * d) * P + p0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g[j] -= T(F4(ua, j)) * k1[j] + T(F4(ub, j)) * k2[j];
+  }
+  {  // last axis: window x(i0-4 .. i0+7)
+    constexpr int d = D - 1;
+    const int n = G.n[d], i0 = idx[d];
+    float w[12];
+    const float4 wl = i0 >= 4 ? ld4(xb + p0 - 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 wm = ld4(xb + p0);
+    const float4 wr = i0 + 4 < n ? ld4(xb + p0 + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      w[j] = F4(wl, j);
+      w[4 + j] = F4(wm, j);
+      w[8 + j] = F4(wr, j);
+    }
+    const float4 ua = ld4(cb + (size_t)(2 + 2 * d) * P + p0), ub = ld4(cb + (size_t)(3 + 2 * d) * P + p0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j;
+      T k1 = 0, k2 = 0;
+      if (i >= 2 && i <= n - 3) {
+#pragma unroll
+        for (int o = -2; o <= 2; ++o) {
+          k1 += T(G.irow[d][(o + 2) * 2]) * T(w[4 + j + o]);
+          k2 += T(G.irow[d][(o + 2) * 2 + 1]) * T(w[4 + j + o]);
+        }
+      } else {
+        const float* row = tab_row(G, d, i);
+#pragma unroll
+        for (int o = -4; o <= 4; ++o) {  // out-of-range taps have zero coefficients
+          if (4 + j + o < 0 || 4 + j + o > 11) continue;
+          k1 += T(__ldg(row + (o + 4) * 2)) * T(w[4 + j + o]);
+          k2 += T(__ldg(row + (o + 4) * 2 + 1)) * T(w[4 + j + o]);
+        }
+      }
+      g[j] -= T(F4(ua, j)) * k1 + T(F4(ub, j)) * k2;
+    }
+  }
+  {
+    const float4 c1 = ld4(cb + P + p0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g[j] *= T(F4(c1, j));
+  }
+}
+
+template <int D, typename T>
+__device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__ cb,
+                                         const float* __restrict__ xb, const T* __restrict__ hb,
+                                         int p0, const int* idx, T* acc) {
+  const int P = G.P;
+  {
+    T h0[4];
+    ldT4<T>(hb + p0, h0);
+    const float4 c0 = ld4(cb + p0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = T(F4(c0, j)) * h0[j];
+    // boundary rows: faces of the non-last axes cover all 4 points; last-axis faces per point
+    bool face = false;
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d) face |= (idx[d] == 0) | (idx[d] == G.n[d] - 1);
+    const float4 x0 = ld4(xb + p0);
+    const T wb2 = T(G.wb) * T(G.wb);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = idx[D - 1] + j;
+      if (face || i == 0 || i == G.n[D - 1] - 1) acc[j] += wb2 * T(F4(x0, j));
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) {
+    const int n = G.n[d], s = G.stride[d], i = idx[d];
+    const float* u1 = cb + (size_t)(2 + 2 * d) * P;
+    const float* u2 = cb + (size_t)(3 + 2 * d) * P;
+    if (i >= 7 && i <= n - 8) {
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        const float4 xv = ld4(xb + p0 + o * s);
+        const T a = G.irow[d][20 + o + 4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] += a * T(F4(xv, j));
+      }
+#pragma unroll
+      for (int o = -2; o <= 2; ++o) {
+        const int q = p0 + o * s;
+        const float4 va = ld4(u1 + q), vb = ld4(u2 + q);
+        T hv[4];
+        ldT4<T>(hb + q, hv);
+        const T a = G.irow[d][10 + (o + 2) * 2], b = G.irow[d][10 + (o + 2) * 2 + 1];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] -= (a * T(F4(va, j)) + b * T(F4(vb, j))) * hv[j];
+      }
+    } else {
+      const float* row = tab_row(G, d, i);
+      for (int o = max(-5, -i); o <= min(5, n - 1 - i); ++o) {
+        const float4 xv = ld4(xb + p0 + o * s);
+        const T a = __ldg(row + 36 + o + 5);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] += a * T(F4(xv, j));
+      }
+      for (int o = max(-4, -i); o <= min(4, n - 1 - i); ++o) {
+        const int q = p0 + o * s;
+        const float4 va = ld4(u1 + q), vb = ld4(u2 + q);
+        T hv[4];
+        ldT4<T>(hb + q, hv);
+        const T a = __ldg(row + 18 + (o + 4) * 2), b = __ldg(row + 18 + (o + 4) * 2 + 1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] -= (a * T(F4(va, j)) + b * T(F4(vb, j))) * hv[j];
+      }
+    }
+  }
+  {  // last axis: x window (i0-8 .. i0+11), u1/u2/h windows (i0-4 .. i0+7)
+    constexpr int d = D - 1;
+    const int n = G.n[d], i0 = idx[d];
+    const float* u1 = cb + (size_t)(2 + 2 * d) * P;
+    const float* u2 = cb + (size_t)(3 + 2 * d) * P;
+    float xw[20];
+    float aw[12], bw[12];
+    T hw[12];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int off = -8 + 4 * k;
+      const bool ok = (i0 + off >= 0) && (i0 + off < n);
+      const float4 v = ok ? ld4(xb + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) xw[4 * k + j] = F4(v, j);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int off = -4 + 4 * k;
+      const bool ok = (i0 + off >= 0) && (i0 + off < n);
+      const float4 va = ok ? ld4(u1 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 vb = ok ? ld4(u2 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+      T hv[4] = {0, 0, 0, 0};
+      if (ok) ldT4<T>(hb + p0 + off, hv);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        aw[4 * k + j] = F4(va, j);
+        bw[4 * k + j] = F4(vb, j);
+        hw[4 * k + j] = hv[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j;
+      if (i >= 7 && i <= n - 8) {
+#pragma unroll
+        for (int o = -4; o <= 4; ++o) acc[j] += T(G.irow[d][20 + o + 4]) * T(xw[8 + j + o]);
+#pragma unroll
+        for (int o = -2; o <= 2; ++o)
+          acc[j] -= (T(G.irow[d][10 + (o + 2) * 2]) * T(aw[4 + j + o]) +
+                     T(G.irow[d][10 + (o + 2) * 2 + 1]) * T(bw[4 + j + o])) * hw[4 + j + o];
+      } else {
+        const float* row = tab_row(G, d, i);
+#pragma unroll
+        for (int o = -5; o <= 5; ++o) acc[j] += T(__ldg(row + 36 + o + 5)) * T(xw[8 + j + o]);
+#pragma unroll
+        for (int o = -4; o <= 4; ++o) {
+          if (4 + j + o < 0 || 4 + j + o > 11) continue;
+          acc[j] -= (T(__ldg(row + 18 + (o + 4) * 2)) * T(aw[4 + j + o]) +
+                     T(__ldg(row + 18 + (o + 4) * 2 + 1)) * T(bw[4 + j + o])) * hw[4 + j + o];
+        }
+      }
+    }
+  }
+}
+
+template <int D, typename T>
+__global__ void __launch_bounds__(kThreads) k_schur_h_v4(Geo G, const float* __restrict__ cf, int crep,
+                                                        const float* __restrict__ x,
+                                                        T* __restrict__ hout, const int* act,
+                                                        unsigned long long* pts) {
+  constexpr int NC = 2 + 2 * D;
+  const int v = blockIdx.y, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (p0 >= P) return;
+  int idx[D];
+  unravel<D>(G, p0, idx);
+  T g[4];
+  schur_h4<D, T>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, p0, idx, g);
+  stT4<T>(hout + (size_t)v * P + p0, g);
+  if (pts && threadIdx.x == 0) atomicAdd(pts, (unsigned long long)min(4 * kThreads, P - p0));
+}
+
+template <int D, int EPI, typename T>
+__global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const float* __restrict__ cf, int crep,
+                                                        const float* __restrict__ x,
+                                                        const T* __restrict__ hb, EpiArgs A,
+                                                        const int* act) {
+  constexpr int NC = 2 + 2 * D;
+  const int v = blockIdx.y, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  double dot = 0.0;
+  if (p0 < P) {
+    int idx[D];
+    unravel<D>(G, p0, idx);
+    const size_t o = (size_t)v * P + p0;
+    T acc[4];
+    schur_s4<D, T>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, hb + (size_t)v * P, p0, idx,
+                   acc);
+    float q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) q[j] = float(acc[j]);
+    if (EPI == EPI_STORE) {
+      st4(A.y + o, q);
+    } else if (EPI == EPI_DOT) {
+      st4(A.y + o, q);
+      const float4 xv = ld4(x + o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dot += double(F4(xv, j)) * q[j];
+    } else if (EPI == EPI_POWER) {
+      const float4 xv = ld4(x + o), dv = ld4(A.dinv + o);
+      float y[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        y[j] = F4(dv, j) * q[j];
+        dot += double(F4(xv, j)) * q[j];
+      }
+      st4(A.y + o, y);
+    } else if (EPI == EPI_RESID) {
+      const float4 rv = ld4(A.res + o);
+      float r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[j] = F4(rv, j) - q[j];
+      st4(A.res + o, r);
+    } else if (EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST) {
+      const float al = A.coef[pde * A.coef_stride + 2 * A.step];
+      const float be = A.coef[pde * A.coef_stride + 2 * A.step + 1];
+      const float4 rv = ld4(A.res + o), xv = ld4(x + o), dv = ld4(A.dinv + o), ev = ld4(A.e + o);
+      float r[4], dn[4], e[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        r[j] = F4(rv, j) - q[j];
+        dn[j] = al * F4(xv, j) + be * F4(dv, j) * r[j];
+        e[j] = F4(ev, j) + dn[j];
+      }
+      st4(A.e + o, e);
+      if (EPI == EPI_SMOOTH) {
+        st4(A.res + o, r);
+        st4(A.d_out + o, dn);
+      }
+      if (A.rdot) {
+        const float4 pv = ld4(A.rdot + o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dot += double(F4(pv, j)) * e[j];
+      }
+    } else if (EPI == EPI_POST0) {
+      const float be = A.coef[pde * A.coef_stride + 1];
+      const float4 rv = ld4(A.res + o), xv = ld4(x + o), dv = ld4(A.dinv + o), ev = ld4(A.e + o);
+      float r[4], dn[4], e[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        r[j] = F4(rv, j) - q[j];
+        dn[j] = be * F4(dv, j) * r[j];
+        e[j] = F4(ev, j) + F4(xv, j) + dn[j];
+      }
+      st4(A.e + o, e);
+      st4(A.res + o, r);
+      st4(A.d_out + o, dn);
+      if (A.rdot) {
+        const float4 pv = ld4(A.rdot + o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dot += double(F4(pv, j)) * e[j];
+      }
+    }
+  }
+  if (A.pts && threadIdx.x == 0 && p0 < P)
+    atomicAdd(A.pts + EPI, (unsigned long long)min(4 * kThreads, P - p0));
+  if (EPI == EPI_DOT || EPI == EPI_POWER ||
+      ((EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST || EPI == EPI_POST0) && A.rdot)) {
+    dot = block_sum(dot);
+    if (threadIdx.x == 0) A.part[(size_t)v * gridDim.x + blockIdx.x] = dot;
+  }
+}
+
+// ------------------------------------------------------------------------- launchers
+static inline dim3 grid2(int P, int nvec) { return dim3((P + kThreads - 1) / kThreads, nvec); }
+
+#define DISPATCH_D2(D_, ...) \
+  do {                       \
+    if ((D_) == 2) {         \
+      constexpr int DD = 2;  \
+      __VA_ARGS__;           \
+    } else {                 \
+      constexpr int DD = 3;  \
+      __VA_ARGS__;           \
+    }                        \
+  } while (0)
+
+void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStream_t s) {
+  ++g_launch_count;
+  DISPATCH_D2(G.D, k_schur_coef<DD><<<grid2(G.P, B), kThreads, 0, s>>>(G, c, cf));
+}
+
+static inline bool use_v4(const Geo& G) { return (G.n[G.D - 1] & 3) == 0; }
+int schur_tiles(const Geo& G) {
+  return use_v4(G) ? (G.P + 4 * kThreads - 1) / (4 * kThreads) : (G.P + kThreads - 1) / kThreads;
+}
+
+void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const float* x, void* g,
+                    const int* act, unsigned long long* pts, bool f64, cudaStream_t s) {
+  ++g_launch_count;
+  if (use_v4(G)) {
+    dim3 gr(schur_tiles(G), nvec);
+    if (f64)
+      DISPATCH_D2(G.D, k_schur_h_v4<DD, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (double*)g, act, pts));
+    else
+      DISPATCH_D2(G.D, k_schur_h_v4<DD, float><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (float*)g, act, pts));
+    return;
+  }
+  if (f64)
+    DISPATCH_D2(G.D, k_schur_h<DD, double><<<grid2(G.P, nvec), kThreads, 0, s>>>(G, cf, crep, x, (double*)g, act, pts));
+  else
+    DISPATCH_D2(G.D, k_schur_h<DD, float><<<grid2(G.P, nvec), kThreads, 0, s>>>(G, cf, crep, x, (float*)g, act, pts));
+}
+
+void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf, const float* x,
+                      const void* g, const EpiArgs& A, const int* act, bool f64, cudaStream_t s) {
+  ++g_launch_count;
+  const bool v4 = use_v4(G);
+  dim3 gr(schur_tiles(G), nvec);
+#define EPI_CASE2(E)                                                                              \
+  case E:                                                                                         \
+    if (v4) {                                                                                     \
+      if (f64)                                                                                    \
+        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const double*)g, A, act)); \
+      else                                                                                        \
+        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, float><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act)); \
+    } else if (f64)                                                                               \
+      DISPATCH_D2(G.D, k_schur_s<DD, E, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const double*)g, A, act)); \
+    else                                                                                          \
+      DISPATCH_D2(G.D, k_schur_s<DD, E, float><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act)); \
+    break;
+  switch (epi) {
+    EPI_CASE2(EPI_STORE)
+    EPI_CASE2(EPI_DOT)
+    EPI_CASE2(EPI_POWER)
+    EPI_CASE2(EPI_RESID)
+    EPI_CASE2(EPI_SMOOTH)
+    EPI_CASE2(EPI_SMOOTH_LAST)
+    EPI_CASE2(EPI_POST0)
+  }
+#undef EPI_CASE2
+}
+
+void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaStream_t s) {
+  ++g_launch_count;
+  DISPATCH_D2(G.D, k_schur_diag<DD><<<grid2(G.P, B), kThreads, 0, s>>>(G, cf, dinv));
+}
+
+}  // namespace mpde

@@ -31,12 +31,13 @@ class mpde_options(C.Structure):
                 ("max_refine", C.c_int32), ("smoother", C.c_int32), ("nu", C.c_int32),
                 ("coarsest", C.c_int32), ("levels_max", C.c_int32), ("poll_every", C.c_int32),
                 ("jacobi_theta", C.c_float), ("cheb_ratio", C.c_float),
-                ("lanczos_steps", C.c_int32), ("precision", C.c_int32)]
+                ("lanczos_steps", C.c_int32), ("precision", C.c_int32),
+                ("use_graphs", C.c_int32), ("tol_z", C.c_float)]
 
 
 class mpde_stats(C.Structure):
     _fields_ = [("iters", C.c_int32), ("refines", C.c_int32), ("status", C.c_int32),
-                ("rel_res", C.c_float)]
+                ("rel_res", C.c_float), ("err_est", C.c_float)]
 
 
 STATUS = {0: "converged", 1: "maxiter", 2: "nonfinite", 3: "indefinite"}
@@ -241,7 +242,7 @@ class Solver:
         self.c = _dev_f32(c, "c")
         nbytes = mpde_workspace_bytes(self.prob, self.opts)
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=c.device)
-        self.stats = torch.zeros((self.B, 4), dtype=torch.int32, device=c.device)
+        self.stats = torch.zeros((self.B, 5), dtype=torch.int32, device=c.device)
         self.h_ = mpde_build_hierarchy(self.prob, self.opts, self.c, self.ws, stream)
 
     def forward(self, b, omega, stream=None):
@@ -262,8 +263,10 @@ class Solver:
         out = []
         for row in s:
             rel = row[3:4].view(torch.float32).item()
+            est = row[4:5].view(torch.float32).item()
             out.append({"iters": int(row[0]), "refines": int(row[1]),
-                        "status": STATUS.get(int(row[2]), str(int(row[2]))), "rel_res": rel})
+                        "status": STATUS.get(int(row[2]), str(int(row[2]))), "rel_res": rel,
+                        "err_est": est})
         return out
 
     def close(self):
