@@ -226,6 +226,25 @@ def run_ours(a):
     ms_step = ms / a.steps
     value = world * B * a.steps / (ms / 1e3)
 
+    # ---- phase breakdown (outside the timed region): build / fwd / bwd, CUDA events ----
+    phases = {}
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    s0 = sets[0]
+    torch.cuda.synchronize()
+    evs[0].record(stream)
+    hh = mpde.mpde_build_hierarchy(prob, opts, s0["c"], ws, stream)
+    evs[1].record(stream)
+    mpde.mpde_solve_fwd(hh, s0["b"], s0["om"], z, stats_f, stream)
+    evs[2].record(stream)
+    mpde.mpde_solve_bwd(hh, s0["b"], z, s0["g"], gc, gb, gw, None, stats_b, stream)
+    evs[3].record(stream)
+    mpde.mpde_batch_sum(gc, gsum, stream)
+    evs[4].record(stream)
+    torch.cuda.synchronize()
+    mpde.mpde_destroy_hierarchy(hh)
+    for k, name in enumerate(["build", "fwd", "bwd", "grad_sum"]):
+        phases[name] = evs[k].elapsed_time(evs[k + 1])
+
     # ---- profiled step (outside the timed region): per-class event times --------------
     mpde.mpde_profile_begin()
     step(0)
@@ -304,6 +323,7 @@ def run_ours(a):
                          "avg_launch_us": 1e3 * so_ms / max(so_n, 1),
                          "share_of_step": so_ms / tot_ms if tot_ms else None},
             "kernels": {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items()},
+            "phases_ms": phases,
             "schur_g": {"achieved_gbs": sg_bytes / (sg_ms * 1e-3) / 1e9 if sg_ms else 0.0},
             "iters": {"fwd_mean": sum(fwd_its) / len(fwd_its), "fwd_max": max(fwd_its),
                       "bwd_mean": sum(bwd_its) / len(bwd_its), "bwd_max": max(bwd_its),

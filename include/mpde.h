@@ -92,8 +92,9 @@ typedef struct {
   float   cheb_ratio;     /* Chebyshev interval [lambda_max/ratio, 1.1 lambda_max]       */
   int32_t lanczos_steps;  /* Lanczos steps (2..32) estimating lambda_max per level+PDE  */
   int32_t precision;  /* arithmetic (storage is fp32): 0 = fp32 everywhere; 1 = fp64 for
-                         the condensation and the PCG operator (default); 2 = fp64 in the
-                         V-cycle too.  The refinement residual is always fp64.          */
+                         the condensation / back-substitution (default); 2 = also the
+                         PCG operator; 3 = also the V-cycle.  The refinement residual and
+                         all dot products are always fp64.                              */
   int32_t use_graphs; /* 1 = replay PCG iterations as a CUDA graph (cached per workspace,
                          problem and options); 0 = plain launches                        */
   float   tol_z;      /* error-based stop: after >= 2 refinement passes, stop when the

@@ -105,6 +105,11 @@ void launch_restrict(const Geo& Gf, const Geo& Gc, int nvec, int nfield, const f
                      float* coarse, const int* act, int crep, cudaStream_t s);
 void launch_prolong(const Geo& Gf, const Geo& Gc, int nvec, const float* coarse, float* fine,
                     const int* act, cudaStream_t s);
+// dense.cu: V-cycle transfers of scalar fields
+void launch_restrict1(const Geo& Gf, const Geo& Gc, int nvec, const float* fine, float* coarse,
+                      const int* act, cudaStream_t s);
+void launch_prolong1(const Geo& Gf, const Geo& Gc, int nvec, const float* coarse, float* fine,
+                     const int* act, cudaStream_t s);
 void launch_smooth_start(int P, int nvec, const float* r, const float* dinv, const float* coef,
                          int coef_stride, float* res, float* d, float* e, const int* act,
                          cudaStream_t s);

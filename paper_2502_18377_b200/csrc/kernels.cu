@@ -559,75 +559,6 @@ __global__ void __launch_bounds__(kThreads) k_identity(int Pc, float* x) {
 }
 
 // ----------------------------------------------------------------------------------
-// Coarsest level: in-place Gauss-Jordan inverse of the SPD matrix S_c (fp64), one CTA
-// per PDE.  a: [B][n][n] double (symmetrised from the probe columns).
-// ----------------------------------------------------------------------------------
-__global__ void k_symmetrize(int n, const float* __restrict__ cols, double* a) {
-  const int b = blockIdx.y;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n * n) return;
-  const int i = k / n, j = k - i * n;
-  const float* cb = cols + (size_t)b * n * n;  // column j stored as vector j: cols[j][i]
-  a[(size_t)b * n * n + k] = 0.5 * (double(cb[(size_t)j * n + i]) + double(cb[(size_t)i * n + j]));
-}
-
-__global__ void __launch_bounds__(1024) k_gauss_jordan(int n, double* a, float* inv) {
-  double* A = a + (size_t)blockIdx.x * n * n;
-  __shared__ double prow[1024];
-  __shared__ double pcol[1024];
-  for (int k = 0; k < n; ++k) {
-    __syncthreads();
-    const double piv = 1.0 / A[(size_t)k * n + k];
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      prow[j] = A[(size_t)k * n + j] * piv;
-      pcol[j] = A[(size_t)j * n + k];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
-      const int i = t / n, j = t - i * n;
-      double val;
-      if (i == k) {
-        val = (j == k) ? piv : prow[j];
-      } else {
-        val = (j == k) ? -pcol[i] * piv : A[t] - pcol[i] * prow[j];
-      }
-      A[t] = val;
-    }
-  }
-  __syncthreads();
-  float* I = inv + (size_t)blockIdx.x * n * n;
-  for (int t = threadIdx.x; t < n * n; t += blockDim.x) I[t] = float(A[t]);
-}
-
-// e = Sinv r (coarsest level), one CTA per (row block, vector); optional dot <rdot, e>
-__global__ void __launch_bounds__(kThreads) k_coarse_gemv(int n, const float* __restrict__ sinv,
-                                                         const float* __restrict__ r, float* e,
-                                                         const float* rdot, double* part,
-                                                         const int* act) {
-  const int v = blockIdx.y;
-  if (act && !act[v]) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = blockDim.x >> 5;
-  const float* S = sinv + (size_t)v * n * n;
-  const float* rv = r + (size_t)v * n;
-  double dot = 0.0;
-  for (int row = blockIdx.x * nw + warp; row < n; row += gridDim.x * nw) {
-    float acc = 0.f;
-    for (int j = lane; j < n; j += 32) acc += S[(size_t)row * n + j] * rv[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      e[(size_t)v * n + row] = acc;
-      if (rdot) dot += double(rdot[(size_t)v * n + row]) * acc;
-    }
-  }
-  if (part) {
-    dot = block_sum(dot);
-    if (threadIdx.x == 0) part[(size_t)v * gridDim.x + blockIdx.x] = dot;
-  }
-}
-
-// ----------------------------------------------------------------------------------
 // Per-PDE scalar logic (one thread per PDE).  Sums the CTA partials in a fixed order
 // (deterministic) and updates the PCG state.
 // ----------------------------------------------------------------------------------
@@ -1077,20 +1008,6 @@ void launch_rand_fill(int P, int nvec, float* y, uint32_t seed, cudaStream_t s) 
 void launch_identity(int Pc, int nvec, float* x, cudaStream_t s) {
   ++g_launch_count;
   k_identity<<<grid_for(Pc, nvec), kThreads, 0, s>>>(Pc, x);
-}
-void launch_coarse_invert(int n, int B, const float* cols, double* scratch, float* inv,
-                          cudaStream_t s) {
-  ++g_launch_count;
-  dim3 g1((n * n + kThreads - 1) / kThreads, B);
-  k_symmetrize<<<g1, kThreads, 0, s>>>(n, cols, scratch);
-  k_gauss_jordan<<<B, 1024, 0, s>>>(n, scratch, inv);
-}
-int coarse_gemv_blocks(int n) { return (n + 7) / 8 < 16 ? (n + 7) / 8 : 16; }
-void launch_coarse_gemv(int n, int nvec, const float* sinv, const float* r, float* e,
-                        const float* rdot, double* part, const int* act, cudaStream_t s) {
-  ++g_launch_count;
-  dim3 g(coarse_gemv_blocks(n), nvec);
-  k_coarse_gemv<<<g, kThreads, 0, s>>>(n, sinv, r, e, rdot, part, act);
 }
 void launch_scalar(int op, int B, const PdeState& st, const double* part, int nt, float tol2,
                    int max_iters, cudaStream_t s) {

@@ -86,8 +86,8 @@ int validate(const mpde_problem* pr, const mpde_options* op) {
     return set_err(MPDE_ERR_INVALID_ARG, "max_refine, max_iters, poll_every must be >= 1");
   if (op->lanczos_steps < 2 || op->lanczos_steps > 32)
     return set_err(MPDE_ERR_INVALID_ARG, "lanczos_steps must be in 2..32");
-  if (op->precision < 0 || op->precision > 2)
-    return set_err(MPDE_ERR_INVALID_ARG, "precision must be 0, 1 or 2");
+  if (op->precision < 0 || op->precision > 3)
+    return set_err(MPDE_ERR_INVALID_ARG, "precision must be in 0..3");
   if (!(op->tol > 0) || !(op->tol_inner > 0) || !(op->tol_z > 0))
     return set_err(MPDE_ERR_INVALID_ARG, "tolerances must be > 0");
   return MPDE_OK;
@@ -336,7 +336,8 @@ struct mpde_hierarchy {
 };
 
 inline bool f64_outer(const mpde_hierarchy* h) { return h->opts.precision >= 1; }
-inline bool f64_vcycle(const mpde_hierarchy* h) { return h->opts.precision >= 2; }
+inline bool f64_pcg(const mpde_hierarchy* h) { return h->opts.precision >= 2; }
+inline bool f64_vcycle(const mpde_hierarchy* h) { return h->opts.precision >= 3; }
 
 namespace {
 
@@ -384,7 +385,7 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
   h->rp = bp.take<float>((size_t)B * P);
   h->p = bp.take<float>((size_t)B * P);
   h->q = bp.take<float>((size_t)B * P);
-  h->part_nt = ntiles(P);
+  h->part_nt = std::max(ntiles(P), coarse_gemv_blocks(Pc));  // partial sums per vector
   h->part = bp.take<double>((size_t)2 * B * h->part_nt + 64);  // 2 slots (backsub)
   h->st.rz = bp.take<double>(B);
   h->st.rr0 = bp.take<double>(B);
@@ -485,10 +486,10 @@ int vcycle(mpde_hierarchy* h, int l, const float* rin, const float* rdot, double
   }
   // residual after pre-smoothing, restrict
   if (int rc = schur_apply(h, l, EPI_RESID, B, 1, dcur, A, act, f64_vcycle(h), s)) return rc;
-  PROF(5, s, launch_restrict(lv.G, lc.G, B, 1, lv.r, lc.r, act, 1, s));
+  PROF(5, s, launch_restrict1(lv.G, lc.G, B, lv.r, lc.r, act, s));
   CKL();
   if (int rc = vcycle(h, l + 1, lc.r, nullptr, nullptr, act, s)) return rc;
-  PROF(5, s, launch_prolong(lv.G, lc.G, B, lc.e, lv.pe, act, s));
+  PROF(5, s, launch_prolong1(lv.G, lc.G, B, lc.e, lv.pe, act, s));
   CKL();
   // post-smoothing: e += P e_c; res -= S (P e_c); d0 = beta0 Dinv res; e += d0
   A.step = 0;
@@ -604,7 +605,7 @@ int pcg(mpde_hierarchy* h, cudaStream_t s) {
     EpiArgs A;
     A.y = h->q;
     A.part = h->part;
-    if (int rc = schur_apply(h, 0, EPI_DOT, B, 1, h->p, A, act, f64_outer(h), st)) return rc;
+    if (int rc = schur_apply(h, 0, EPI_DOT, B, 1, h->p, A, act, f64_pcg(h), st)) return rc;
     PROF(7, st, launch_scalar(SC_ALPHA, B, h->st, h->part, nts, tol2, h->opts.max_iters, st));
     PROF(6, st, launch_pcg_update(P, B, h->st.alpha, h->p, h->q, h->x, h->rp, h->part, act, st));
     PROF(7, st, launch_scalar(SC_CONV, B, h->st, h->part, nt, tol2, h->opts.max_iters, st));
@@ -749,11 +750,25 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
                    "coarsest level has %d points (> %d); raise levels_max / lower coarsest",
                    h->Pc, kMaxCoarse);
   }
-  if (cudaHostAlloc(&h->h_count, 2 * sizeof(int), cudaHostAllocDefault) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev[0], cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev[1], cudaEventDisableTiming) != cudaSuccess) {
-    delete h;
-    return set_err(MPDE_ERR_CUDA, "cudaHostAlloc failed");
+  {
+    // per-thread pinned poll slots and events, created once (a cudaHostAlloc per build
+    // would cost milliseconds and its free would synchronise the device)
+    struct PollRes {
+      int* pinned = nullptr;
+      cudaEvent_t ev[2] = {nullptr, nullptr};
+    };
+    static thread_local PollRes pr;
+    if (!pr.pinned) {
+      if (cudaHostAlloc(&pr.pinned, 2 * sizeof(int), cudaHostAllocDefault) != cudaSuccess ||
+          cudaEventCreateWithFlags(&pr.ev[0], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&pr.ev[1], cudaEventDisableTiming) != cudaSuccess) {
+        delete h;
+        return set_err(MPDE_ERR_CUDA, "cudaHostAlloc / cudaEventCreate failed");
+      }
+    }
+    h->h_count = pr.pinned;
+    h->ev[0] = pr.ev[0];
+    h->ev[1] = pr.ev[1];
   }
   h->st.tol = opts->tol;
   h->st.tol_z = opts->tol_z;
@@ -852,10 +867,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
 
 int mpde_destroy_hierarchy(mpde_hierarchy* h) {
   if (!h) return MPDE_OK;
-  if (h->h_count) cudaFreeHost(h->h_count);
-  if (h->ev[0]) cudaEventDestroy(h->ev[0]);
-  if (h->ev[1]) cudaEventDestroy(h->ev[1]);
-  delete h;
+  delete h;  // poll slots / events are per-thread resources, reused by the next handle
   return MPDE_OK;
 }
 
@@ -910,7 +922,7 @@ int mpde_apply_schur(mpde_hierarchy* h, int32_t level, const float* x, float* y,
   if (level < 0 || level >= h->L) return set_err(MPDE_ERR_INVALID_ARG, "bad level %d", level);
   EpiArgs A;
   A.y = y;
-  return schur_apply(h, level, EPI_STORE, h->B, 1, x, A, nullptr, f64_outer(h),
+  return schur_apply(h, level, EPI_STORE, h->B, 1, x, A, nullptr, f64_pcg(h),
                      (cudaStream_t)stream_);
 }
 
