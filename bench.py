@@ -100,39 +100,43 @@ def _oracle_sample(args):
     t0 = time.perf_counter()
     A, d, _ = assemble(pr, c.reshape(M, -1).astype(np.float32), b.reshape(-1).astype(np.float32),
                        om.reshape(-1).astype(np.float32))
-    t1 = time.perf_counter()
-    est = t1 - t0
-    spent = t1 - t0
-    for rhs in (A.T @ d, np.random.default_rng(idx).standard_normal(A.shape[1])):
-        info = {}
-        ts = time.perf_counter()
-        solve_normal(A, rhs, method="cg", tol=1e-12, maxiter=cap, info=info)
-        dt = time.perf_counter() - ts
-        spent += dt
-        it = max(1, info.get("iters", cap))
-        rel = max(info.get("rel_res", 1.0), 1e-300)
-        if rel <= 1e-12:
-            est += dt
-        else:
-            rate = rel ** (1.0 / it)
-            need = np.log(1e-12) / np.log(rate) if rate < 1 else float("inf")
-            est += dt / it * max(need, it)
-    return spent, est
+    t_asm = time.perf_counter() - t0
+    info = {}
+    ts = time.perf_counter()
+    solve_normal(A, A.T @ d, method="cg", tol=1e-12, maxiter=cap, info=info)
+    t_it = (time.perf_counter() - ts) / max(1, info.get("iters", cap))
+    return t_asm, t_it
 
 
-def cpu_oracle_baseline(cap=300, workers=None):
+# Iterations the oracle's Jacobi-CG needs to its 1e-12 stop on a C4 PDE, measured by
+# tools/oracle_c4_iters.py (full oracle solves; profiles/oracle_c4_iters.json).
+def _oracle_iters():
+    try:
+        with open(os.path.join(ROOT, "profiles", "oracle_c4_iters.json")) as f:
+            j = json.load(f)
+        fi = j["fwd"]["iters"]
+        return fi, j.get("bwd", {}).get("iters", fi)
+    except Exception:
+        return 6649, 6649
+
+
+def cpu_oracle_baseline(cap=200, workers=None):
     import multiprocessing as mp
     n = workers or min(8, os.cpu_count() or 1)
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(n) as pool:
         res = pool.map(_oracle_sample, [(i, cap) for i in range(n)])
     wall = time.perf_counter() - t0
-    est = sum(r[1] for r in res) / len(res)     # extrapolated seconds per fwd+bwd solve
+    i_f, i_b = _oracle_iters()
+    t_asm = sum(r[0] for r in res) / len(res)
+    t_it = sum(r[1] for r in res) / len(res)
+    est = t_asm + t_it * (i_f + i_b)  # seconds per fwd+bwd solve, one core
     return {"value": n / est, "unit": "PDE solves/s (fwd+bwd)", "cores": n, "kind": "oracle",
-            "sample": (f"{n} PDEs of {CFG} (32x64x64, NS vorticity) on {n} processes x 1 thread: "
-                       f"oracle assembly + fp64 Jacobi-CG fwd and bwd capped at {cap} iterations "
-                       f"each, extrapolated to the oracle's 1e-12 stop at the observed "
-                       f"contraction; {wall:.1f}s wall")}, wall
+            "sample": (f"{n} C4 PDEs (32x64x64, NS vorticity) on {n} processes x 1 thread: oracle "
+                       f"assembly ({t_asm:.2f} s) + {cap} fp64 Jacobi-CG iterations "
+                       f"({1e3 * t_it:.1f} ms each), scaled to the {i_f} + {i_b} iterations the "
+                       f"oracle needs for fwd + bwd (full runs, profiles/oracle_c4_iters.json); "
+                       f"{wall:.1f}s wall")}, wall
 
 
 # ------------------------------------------------------------------------------ ours

@@ -297,10 +297,13 @@ __device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__
           k2[j] += b * T(F4(xv, j));
         }
       }
-    } else {
+    } else {  // edge rows: unrolled, clamped addresses, zero coefficients out of range
       const float* row = tab_row(G, d, i);
-      for (int o = max(-4, -i); o <= min(4, n - 1 - i); ++o) {
-        const float4 xv = ld4(xb + p0 + o * s);
+      const int olo = -i, ohi = n - 1 - i;
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        const int oc = o < olo ? olo : (o > ohi ? ohi : o);
+        const float4 xv = ld4(xb + p0 + oc * s);
         const T a = __ldg(row + (o + 4) * 2), b = __ldg(row + (o + 4) * 2 + 1);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -403,15 +406,22 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
         for (int j = 0; j < 4; ++j) acc[j] -= (a * T(F4(va, j)) + b * T(F4(vb, j))) * hv[j];
       }
     } else {
+      // edge classes: fully unrolled, addresses clamped into the line (the table holds
+      // zero coefficients for out-of-range taps) so that every load issues at once
       const float* row = tab_row(G, d, i);
-      for (int o = max(-5, -i); o <= min(5, n - 1 - i); ++o) {
-        const float4 xv = ld4(xb + p0 + o * s);
+      const int olo = -i, ohi = n - 1 - i;
+#pragma unroll
+      for (int o = -5; o <= 5; ++o) {
+        const int oc = o < olo ? olo : (o > ohi ? ohi : o);
+        const float4 xv = ld4(xb + p0 + oc * s);
         const T a = __ldg(row + 36 + o + 5);
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[j] += a * T(F4(xv, j));
       }
-      for (int o = max(-4, -i); o <= min(4, n - 1 - i); ++o) {
-        const int q = p0 + o * s;
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        const int oc = o < olo ? olo : (o > ohi ? ohi : o);
+        const int q = p0 + oc * s;
         const float4 va = ld4(u1 + q), vb = ld4(u2 + q);
         T hv[4];
         ldT4<T>(hb + q, hv);
