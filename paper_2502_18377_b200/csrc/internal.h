@@ -99,7 +99,7 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* c,
 // schur.cu: cf = per-point coefficients [B][2+2D][P] of S (from c), dinv = 1/diag(S)
 void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStream_t s);
 // number of CTAs (= partial sums per vector) of the S kernels on this level
-int schur_tiles(const Geo& G);
+int schur_tiles(const Geo& G, bool f64);
 void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaStream_t s);
 void launch_restrict(const Geo& Gf, const Geo& Gc, int nvec, int nfield, const float* fine,
                      float* coarse, const int* act, int crep, cudaStream_t s);

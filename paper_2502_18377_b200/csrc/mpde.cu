@@ -585,8 +585,9 @@ __global__ void k_dot_self(int P, const float* __restrict__ r, double* part, con
 int pcg(mpde_hierarchy* h, cudaStream_t s) {
   const int B = h->B, P = h->P;
   const int nt = ntiles(P);                  // partials of the pointwise vector kernels
-  const int nts = schur_tiles(h->lv[0].G);   // partials of the S kernels
-  const int ntc = h->L == 1 ? coarse_gemv_blocks(h->Pc) : nts;
+  const int nts = schur_tiles(h->lv[0].G, f64_pcg(h));   // partials of the PCG S kernel
+  const int ntc = h->L == 1 ? coarse_gemv_blocks(h->Pc)  // ... of the V-cycle's last kernel
+                            : schur_tiles(h->lv[0].G, f64_vcycle(h));
   const float tol2 = h->opts.tol_inner * h->opts.tol_inner;
   const int* act = h->st.act;
   Level& l0 = h->lv[0];
@@ -695,7 +696,7 @@ mpde_options mpde_default_options(void) {
   o.levels_max = 8;
   o.poll_every = 8;
   o.jacobi_theta = 1.3f;
-  o.cheb_ratio = 30.f;
+  o.cheb_ratio = 60.f;
   o.lanczos_steps = 16;
   o.precision = 1;
   o.use_graphs = 1;
@@ -829,7 +830,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
         delete h;
         return rc;
       }
-      launch_scalar(SC_LZ_ALPHA, B, sl, h->part, schur_tiles(lv.G), 0.f, j, s);
+      launch_scalar(SC_LZ_ALPHA, B, sl, h->part, schur_tiles(lv.G, f64_vcycle(h)), 0.f, j, s);
       launch_lz_update(lv.P, B, y, v, vp, lv.dinv, h->st.alpha, h->st.beta, h->part, s);
       launch_scalar(SC_LZ_BETA, B, sl, h->part, nt, 0.f, j, s);
       launch_scale(lv.P, B, h->st.alpha, vp, vp, h->ones, s);

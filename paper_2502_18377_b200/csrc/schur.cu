@@ -17,6 +17,8 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <cstdlib>
+
 namespace mpde {
 
 template <int D>
@@ -597,6 +599,328 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const float* __r
   }
 }
 
+// ---------------------------------------------------------------------------------
+// 3D pass 2 with 2x2 register blocking in (t, x): a thread computes the four y-quads at
+// (t0+a, x0+b), a, b in {0,1}.  Every t- (x-) neighbour load feeds both t (x) outputs,
+// which cuts the L1 gathers per quad by ~30% (the v4 kernel is L1-wavefront bound).
+// ---------------------------------------------------------------------------------
+template <int AX>  // accumulate the AX-axis (0 = t, 1 = x) terms of a 2-output pencil
+__device__ __forceinline__ void pencil2(const Geo& G, const float* __restrict__ cb,
+                                        const float* __restrict__ xb, const float* __restrict__ hb,
+                                        int pbase, int i0, bool ok1, float* acc0, float* acc1) {
+  // pbase: offset of output 0 (index i0 along AX); output 1 is at pbase + s (index i0+1)
+  const int P = G.P, n = G.n[AX], s = G.stride[AX];
+  const float* u1 = cb + (size_t)(2 + 2 * AX) * P;
+  const float* u2 = cb + (size_t)(3 + 2 * AX) * P;
+  if (i0 >= 7 && i0 + 1 <= n - 8) {
+#pragma unroll
+    for (int u = -4; u <= 5; ++u) {
+      const float4 xv = ld4(xb + pbase + u * s);
+      const float c0 = u <= 4 ? G.irow[AX][20 + u + 4] : 0.f;
+      const float c1 = u >= -3 ? G.irow[AX][20 + u - 1 + 4] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc0[j] += c0 * F4(xv, j);
+        acc1[j] += c1 * F4(xv, j);
+      }
+    }
+#pragma unroll
+    for (int u = -2; u <= 3; ++u) {
+      const int q = pbase + u * s;
+      const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
+      const float a0 = u <= 2 ? G.irow[AX][10 + (u + 2) * 2] : 0.f;
+      const float b0 = u <= 2 ? G.irow[AX][10 + (u + 2) * 2 + 1] : 0.f;
+      const float a1 = u >= -1 ? G.irow[AX][10 + (u + 1) * 2] : 0.f;
+      const float b1 = u >= -1 ? G.irow[AX][10 + (u + 1) * 2 + 1] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float w0 = (a0 * F4(va, j) + b0 * F4(vb, j)) * F4(hv, j);
+        const float w1 = (a1 * F4(va, j) + b1 * F4(vb, j)) * F4(hv, j);
+        acc0[j] -= w0;
+        acc1[j] -= w1;
+      }
+    }
+    return;
+  }
+  // edge classes: table rows per output, clamped addresses, zero coefficients out of range
+  const float* r0 = tab_row(G, AX, i0);
+  const float* r1 = tab_row(G, AX, ok1 ? i0 + 1 : i0);
+  const float m1 = ok1 ? 1.f : 0.f;
+#pragma unroll
+  for (int u = -5; u <= 6; ++u) {
+    const int ic = min(max(i0 + u, 0), n - 1);
+    const float4 xv = ld4(xb + pbase + (ic - i0) * s);
+    const float c0 = u <= 5 ? __ldg(r0 + 36 + u + 5) : 0.f;
+    const float c1 = u >= -4 ? m1 * __ldg(r1 + 36 + u - 1 + 5) : 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      acc0[j] += c0 * F4(xv, j);
+      acc1[j] += c1 * F4(xv, j);
+    }
+  }
+#pragma unroll
+  for (int u = -4; u <= 5; ++u) {
+    const int ic = min(max(i0 + u, 0), n - 1);
+    const int q = pbase + (ic - i0) * s;
+    const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
+    const float a0 = u <= 4 ? __ldg(r0 + 18 + (u + 4) * 2) : 0.f;
+    const float b0 = u <= 4 ? __ldg(r0 + 18 + (u + 4) * 2 + 1) : 0.f;
+    const float a1 = u >= -3 ? m1 * __ldg(r1 + 18 + (u + 3) * 2) : 0.f;
+    const float b1 = u >= -3 ? m1 * __ldg(r1 + 18 + (u + 3) * 2 + 1) : 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      acc0[j] -= (a0 * F4(va, j) + b0 * F4(vb, j)) * F4(hv, j);
+      acc1[j] -= (a1 * F4(va, j) + b1 * F4(vb, j)) * F4(hv, j);
+    }
+  }
+}
+
+// one-output version of pencil2 (single quad, AX-axis terms)
+template <int AX>
+__device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ cb,
+                                        const float* __restrict__ xb, const float* __restrict__ hb,
+                                        int p0, int i, float* acc) {
+  const int P = G.P, n = G.n[AX], s = G.stride[AX];
+  const float* u1 = cb + (size_t)(2 + 2 * AX) * P;
+  const float* u2 = cb + (size_t)(3 + 2 * AX) * P;
+  if (i >= 7 && i <= n - 8) {
+#pragma unroll
+    for (int o = -4; o <= 4; ++o) {
+      const float4 xv = ld4(xb + p0 + o * s);
+      const float a = G.irow[AX][20 + o + 4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] += a * F4(xv, j);
+    }
+#pragma unroll
+    for (int o = -2; o <= 2; ++o) {
+      const int q = p0 + o * s;
+      const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
+      const float a = G.irow[AX][10 + (o + 2) * 2], b = G.irow[AX][10 + (o + 2) * 2 + 1];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] -= (a * F4(va, j) + b * F4(vb, j)) * F4(hv, j);
+    }
+    return;
+  }
+  const float* row = tab_row(G, AX, i);
+  const int olo = -i, ohi = n - 1 - i;
+#pragma unroll
+  for (int o = -5; o <= 5; ++o) {
+    const int oc = o < olo ? olo : (o > ohi ? ohi : o);
+    const float4 xv = ld4(xb + p0 + oc * s);
+    const float a = __ldg(row + 36 + o + 5);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] += a * F4(xv, j);
+  }
+#pragma unroll
+  for (int o = -4; o <= 4; ++o) {
+    const int oc = o < olo ? olo : (o > ohi ? ohi : o);
+    const int q = p0 + oc * s;
+    const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
+    const float a = __ldg(row + 18 + (o + 4) * 2), b = __ldg(row + 18 + (o + 4) * 2 + 1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] -= (a * F4(va, j) + b * F4(vb, j)) * F4(hv, j);
+  }
+}
+
+// y-axis (contiguous) terms + own terms of one quad, as in schur_s4
+__device__ __forceinline__ void quad_y_own(const Geo& G, const float* __restrict__ cb,
+                                           const float* __restrict__ xb,
+                                           const float* __restrict__ hb, int p0, int t, int xr,
+                                           float* acc) {
+  const int P = G.P, n = G.n[2], i0 = p0 % n;
+  {
+    const float4 h0 = ld4(hb + p0), c0 = ld4(cb + p0), x0 = ld4(xb + p0);
+    const bool face = (t == 0) | (t == G.n[0] - 1) | (xr == 0) | (xr == G.n[1] - 1);
+    const float wb2 = G.wb * G.wb;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      acc[j] += F4(c0, j) * F4(h0, j);
+      if (face || i0 + j == 0 || i0 + j == n - 1) acc[j] += wb2 * F4(x0, j);
+    }
+  }
+  const float* u1 = cb + (size_t)6 * P;
+  const float* u2 = cb + (size_t)7 * P;
+  float xw[20], aw[12], bw[12], hw[12];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int off = -8 + 4 * k;
+    const bool ok = (i0 + off >= 0) && (i0 + off < n);
+    const float4 vv = ok ? ld4(xb + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xw[4 * k + j] = F4(vv, j);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int off = -4 + 4 * k;
+    const bool ok = (i0 + off >= 0) && (i0 + off < n);
+    const float4 va = ok ? ld4(u1 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 vb = ok ? ld4(u2 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 hv = ok ? ld4(hb + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      aw[4 * k + j] = F4(va, j);
+      bw[4 * k + j] = F4(vb, j);
+      hw[4 * k + j] = F4(hv, j);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int i = i0 + j;
+    if (i >= 7 && i <= n - 8) {
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) acc[j] += G.irow[2][20 + o + 4] * xw[8 + j + o];
+#pragma unroll
+      for (int o = -2; o <= 2; ++o)
+        acc[j] -= (G.irow[2][10 + (o + 2) * 2] * aw[4 + j + o] +
+                   G.irow[2][10 + (o + 2) * 2 + 1] * bw[4 + j + o]) * hw[4 + j + o];
+    } else {
+      const float* row = tab_row(G, 2, i);
+#pragma unroll
+      for (int o = -5; o <= 5; ++o) acc[j] += __ldg(row + 36 + o + 5) * xw[8 + j + o];
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        if (4 + j + o < 0 || 4 + j + o > 11) continue;
+        acc[j] -= (__ldg(row + 18 + (o + 4) * 2) * aw[4 + j + o] +
+                   __ldg(row + 18 + (o + 4) * 2 + 1) * bw[4 + j + o]) * hw[4 + j + o];
+      }
+    }
+  }
+}
+
+template <int EPI>
+__device__ __forceinline__ double quad_epilogue(const EpiArgs& A, int pde, size_t o,
+                                                const float* __restrict__ x, const float* q) {
+  double dot = 0.0;
+  if (EPI == EPI_STORE) {
+    st4(A.y + o, q);
+  } else if (EPI == EPI_DOT) {
+    st4(A.y + o, q);
+    const float4 xv = ld4(x + o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dot += double(F4(xv, j)) * q[j];
+  } else if (EPI == EPI_POWER) {
+    const float4 xv = ld4(x + o), dv = ld4(A.dinv + o);
+    float y[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      y[j] = F4(dv, j) * q[j];
+      dot += double(F4(xv, j)) * q[j];
+    }
+    st4(A.y + o, y);
+  } else if (EPI == EPI_RESID) {
+    const float4 rv = ld4(A.res + o);
+    float r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r[j] = F4(rv, j) - q[j];
+    st4(A.res + o, r);
+  } else if (EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST) {
+    const float al = A.coef[pde * A.coef_stride + 2 * A.step];
+    const float be = A.coef[pde * A.coef_stride + 2 * A.step + 1];
+    const float4 rv = ld4(A.res + o), xv = ld4(x + o), dv = ld4(A.dinv + o), ev = ld4(A.e + o);
+    float r[4], dn[4], e[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      r[j] = F4(rv, j) - q[j];
+      dn[j] = al * F4(xv, j) + be * F4(dv, j) * r[j];
+      e[j] = F4(ev, j) + dn[j];
+    }
+    st4(A.e + o, e);
+    if (EPI == EPI_SMOOTH) {
+      st4(A.res + o, r);
+      st4(A.d_out + o, dn);
+    }
+    if (A.rdot) {
+      const float4 pv = ld4(A.rdot + o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dot += double(F4(pv, j)) * e[j];
+    }
+  } else if (EPI == EPI_POST0) {
+    const float be = A.coef[pde * A.coef_stride + 1];
+    const float4 rv = ld4(A.res + o), xv = ld4(x + o), dv = ld4(A.dinv + o), ev = ld4(A.e + o);
+    float r[4], dn[4], e[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      r[j] = F4(rv, j) - q[j];
+      dn[j] = be * F4(dv, j) * r[j];
+      e[j] = F4(ev, j) + F4(xv, j) + dn[j];
+    }
+    st4(A.e + o, e);
+    st4(A.res + o, r);
+    st4(A.d_out + o, dn);
+    if (A.rdot) {
+      const float4 pv = ld4(A.rdot + o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dot += double(F4(pv, j)) * e[j];
+    }
+  }
+  return dot;
+}
+
+template <int EPI, int BX>
+__global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __restrict__ cf, int crep,
+                                                         const float* __restrict__ x,
+                                                         const float* __restrict__ hb, EpiArgs A,
+                                                         const int* act) {
+  // BX = 1: 2x2 blocking in (t, x); BX = 0: 2x1 blocking in t only (fewer registers)
+  const int v = blockIdx.y, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  const int nt = G.n[0], nx = G.n[1], ny = G.n[2];
+  const int NY4 = ny >> 2, NXB = BX ? (nx + 1) >> 1 : nx, NT2 = (nt + 1) >> 1;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int yq = tid % NY4, r2 = tid / NY4, xp = r2 % NXB, tp = r2 / NXB;
+  double dot = 0.0;
+  int nq = 0;
+  if (tp < NT2) {
+    const float* cb = cf + (size_t)pde * 8 * P;
+    const float* xb = x + (size_t)v * P;
+    const float* hv = hb + (size_t)v * P;
+    const int t0 = 2 * tp, x0 = BX ? 2 * xp : xp;
+    const bool okt = t0 + 1 < nt, okx = BX && (x0 + 1 < nx);
+    const int st = G.stride[0], sxs = G.stride[1];
+    const int pb = t0 * st + x0 * sxs + 4 * yq;
+    float acc[2][BX + 1][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < BX + 1; ++b)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[a][b][j] = 0.f;
+    // t pencils (columns x0 [, x0+1]) and x terms (planes t0, t0+1)
+    pencil2<0>(G, cb, xb, hv, pb, t0, okt, acc[0][0], acc[1][0]);
+    if (BX) {
+      if (okx) pencil2<0>(G, cb, xb, hv, pb + sxs, t0, okt, acc[0][BX], acc[1][BX]);
+      pencil2<1>(G, cb, xb, hv, pb, x0, okx, acc[0][0], acc[0][BX]);
+      if (okt) pencil2<1>(G, cb, xb, hv, pb + st, x0, okx, acc[1][0], acc[1][BX]);
+    } else {
+      pencil1<1>(G, cb, xb, hv, pb, x0, acc[0][0]);
+      if (okt) pencil1<1>(G, cb, xb, hv, pb + st, x0, acc[1][0]);
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < BX + 1; ++b) {
+        if ((a && !okt) || (b && !okx)) continue;
+        const int p0 = pb + a * st + b * sxs;
+        quad_y_own(G, cb, xb, hv, p0, t0 + a, x0 + b, acc[a][b]);
+        dot += quad_epilogue<EPI>(A, pde, (size_t)v * P + p0, x, acc[a][b]);
+        ++nq;
+      }
+  }
+  if (A.pts) {
+    __shared__ int sq;
+    if (threadIdx.x == 0) sq = 0;
+    __syncthreads();
+    if (nq) atomicAdd(&sq, 4 * nq);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(A.pts + EPI, (unsigned long long)sq);
+  }
+  if (EPI == EPI_DOT || EPI == EPI_POWER ||
+      ((EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST || EPI == EPI_POST0) && A.rdot)) {
+    dot = block_sum(dot);
+    if (threadIdx.x == 0) A.part[(size_t)v * gridDim.x + blockIdx.x] = dot;
+  }
+}
+
 // ------------------------------------------------------------------------- launchers
 static inline dim3 grid2(int P, int nvec) { return dim3((P + kThreads - 1) / kThreads, nvec); }
 
@@ -617,7 +941,24 @@ void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStrea
 }
 
 static inline bool use_v4(const Geo& G) { return (G.n[G.D - 1] & 3) == 0; }
-int schur_tiles(const Geo& G) {
+// 2x2 (t,x)-blocked pass 2: 3D, fp32, n_y % 4 == 0
+static int g_block_mode = -1;  // 0: v4, 1: 2x1 (t), 2: 2x2 (t,x); env MPDE_SCHUR_BLOCK
+static inline int block_mode() {
+  if (g_block_mode < 0) {
+    const char* e = getenv("MPDE_SCHUR_BLOCK");
+    g_block_mode = e ? atoi(e) : 1;
+  }
+  return g_block_mode;
+}
+static inline bool use_b22(const Geo& G, bool f64) {
+  return G.D == 3 && !f64 && use_v4(G) && block_mode() > 0;
+}
+static inline int b22_threads(const Geo& G) {
+  const int bx = block_mode() == 2;
+  return ((G.n[0] + 1) / 2) * (bx ? (G.n[1] + 1) / 2 : G.n[1]) * (G.n[2] / 4);
+}
+int schur_tiles(const Geo& G, bool f64) {
+  if (use_b22(G, f64)) return (b22_threads(G) + kThreads - 1) / kThreads;
   return use_v4(G) ? (G.P + 4 * kThreads - 1) / (4 * kThreads) : (G.P + kThreads - 1) / kThreads;
 }
 
@@ -625,7 +966,7 @@ void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const flo
                     const int* act, unsigned long long* pts, bool f64, cudaStream_t s) {
   ++g_launch_count;
   if (use_v4(G)) {
-    dim3 gr(schur_tiles(G), nvec);
+    dim3 gr((G.P + 4 * kThreads - 1) / (4 * kThreads), nvec);
     if (f64)
       DISPATCH_D2(G.D, k_schur_h_v4<DD, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (double*)g, act, pts));
     else
@@ -641,8 +982,29 @@ void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const flo
 void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf, const float* x,
                       const void* g, const EpiArgs& A, const int* act, bool f64, cudaStream_t s) {
   ++g_launch_count;
+  if (use_b22(G, f64)) {
+    const dim3 gb(schur_tiles(G, f64), nvec);
+#define B22_CASE(E)                                                                          \
+  case E:                                                                                    \
+    if (block_mode() == 2)                                                                   \
+      k_schur_s_b22<E, 1><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act);  \
+    else                                                                                     \
+      k_schur_s_b22<E, 0><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act);  \
+    break;
+    switch (epi) {
+      B22_CASE(EPI_STORE)
+      B22_CASE(EPI_DOT)
+      B22_CASE(EPI_POWER)
+      B22_CASE(EPI_RESID)
+      B22_CASE(EPI_SMOOTH)
+      B22_CASE(EPI_SMOOTH_LAST)
+      B22_CASE(EPI_POST0)
+    }
+#undef B22_CASE
+    return;
+  }
   const bool v4 = use_v4(G);
-  dim3 gr(schur_tiles(G), nvec);
+  dim3 gr(schur_tiles(G, f64), nvec);
 #define EPI_CASE2(E)                                                                              \
   case E:                                                                                         \
     if (v4) {                                                                                     \

@@ -1,0 +1,69 @@
+"""GPU unit tests of the condensed operator paths at sizes that select each kernel variant
+(scalar, 4-points-per-thread, 2x2-blocked) against the dense Schur complement built from the
+oracle's A, and symmetry / positivity of the V-cycle preconditioner."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import Problem, assemble
+
+pytestmark = pytest.mark.gpu
+
+
+def _dense_schur(pr, c):
+    A, _, _ = assemble(pr, c, np.zeros(pr.P), np.zeros(pr.P))
+    N = (A.T @ A).toarray()
+    P = pr.P
+    return N[:P, :P] - N[:P, P:] @ np.linalg.solve(N[P:, P:], N[P:, :P])
+
+
+@pytest.mark.parametrize("shape,h", [((9, 10, 12), (0.1, 0.08, 0.05)),    # v4 (n_y % 4 == 0)
+                                     ((15, 17, 16), (0.05, 0.06, 0.07)),  # 2x2 blocked, odd t/x
+                                     ((16, 18, 20), (0.05, 0.06, 0.07)),  # 2x2 blocked, interior
+                                     ((8, 9, 11), (0.1, 0.1, 0.1)),       # scalar path
+                                     ((20, 24), (0.05, 0.04))])           # 2D v4
+def test_schur_variants_match_dense(shape, h):
+    from paper_2502_18377_b200 import mpde
+    rng = np.random.default_rng(5)
+    D = len(shape)
+    M, P, B = 1 + 2 * D, int(np.prod(shape)), 2
+    c = rng.normal(0.0, 0.5, (B, M, P))
+    c[:, 1] += 1.0
+    c = c.astype(np.float32)
+    w = (1.25, 2.0, 0.75, 0.875)
+    s = mpde.Solver(shape, h, torch.from_numpy(c).cuda(), weights=w,
+                    opts=mpde.mpde_default_options(levels_max=2))
+    x = rng.normal(size=(B, P)).astype(np.float32)
+    y = torch.empty((B, P), dtype=torch.float32, device="cuda")
+    mpde.mpde_apply_schur(s.h_, 0, torch.from_numpy(x).cuda(), y)
+    torch.cuda.synchronize()
+    pr = Problem(shape, h, *w)
+    for i in range(B):
+        S = _dense_schur(pr, c[i].astype(np.float64))
+        ref = S @ x[i]
+        assert np.linalg.norm(y[i].cpu().numpy() - ref) <= 1e-4 * np.linalg.norm(ref)
+    s.close()
+
+
+@pytest.mark.parametrize("shape,h", [((16, 18, 20), (0.05, 0.06, 0.07)), ((20, 24), (0.05, 0.04))])
+def test_vcycle_symmetric_positive(shape, h):
+    """The V-cycle is a fixed SPD linear map (needed by PCG): <Ma, b> = <a, Mb>, <Ma, a> > 0."""
+    from paper_2502_18377_b200 import mpde
+    rng = np.random.default_rng(6)
+    D = len(shape)
+    M, P, B = 1 + 2 * D, int(np.prod(shape)), 2
+    c = rng.normal(0.0, 0.5, (B, M, P))
+    c[:, 1] += 1.0
+    s = mpde.Solver(shape, h, torch.from_numpy(c.astype(np.float32)).cuda())
+    a = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()
+    b = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()
+    ma, mb = torch.empty_like(a), torch.empty_like(b)
+    mpde.mpde_apply_precond(s.h_, a, ma)
+    mpde.mpde_apply_precond(s.h_, b, mb)
+    torch.cuda.synchronize()
+    for i in range(B):
+        l = float((ma[i].double() * b[i].double()).sum())
+        r = float((a[i].double() * mb[i].double()).sum())
+        assert abs(l - r) <= 1e-4 * (abs(l) + abs(r))
+        assert float((ma[i].double() * a[i].double()).sum()) > 0
+    s.close()
