@@ -16,7 +16,10 @@ namespace mpde {
 
 constexpr int kMaxD = 3;
 constexpr int kThreads = 256;
-constexpr int kTabRow = 48;  // floats per (axis, index) row of the condensed-operator tables
+constexpr int kTabRow = 52;  // floats per (axis, index) row of the condensed-operator tables
+constexpr int kTabKf = 0;   // row segments, 16-byte aligned: Kf [0,18), KT [20,38), P0 [40,51)
+constexpr int kTabKT = 20;
+constexpr int kTabP0 = 40;
 
 // Per-level geometry, passed by value to every kernel.
 struct Geo {

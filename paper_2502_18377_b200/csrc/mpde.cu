@@ -227,7 +227,7 @@ void append_axis_tables(int n, double h, double wr, double ws, std::vector<float
     for (int o = -4; o <= 4; ++o)
       for (int k = 0; k < 2; ++k) {
         row[(o + 4) * 2 + k] = float(kcv(k, i, i + o));         // Kf
-        row[18 + (o + 4) * 2 + k] = float(kcv(k, i + o, i));    // KT
+        row[kTabKT + (o + 4) * 2 + k] = float(kcv(k, i + o, i));    // KT
       }
     for (int o = -5; o <= 5; ++o) {
       const int j = i + o;
@@ -243,7 +243,7 @@ void append_axis_tables(int n, double h, double wr, double ws, std::vector<float
         if (ip <= n - 2) v += ws2 * ((i == ip) - (i == ip + 1)) * ((j == ip) - (j == ip + 1));
         if (ip >= 1) v += ws2 * ((i == ip) - (i == ip - 1)) * ((j == ip) - (j == ip - 1));
       }
-      row[36 + o + 5] = float(v);
+      row[kTabP0 + o + 5] = float(v);
     }
   }
 }
@@ -800,9 +800,9 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
       for (int o = -2; o <= 2; ++o)
         for (int k = 0; k < 2; ++k) {
           lv.G.irow[d][(o + 2) * 2 + k] = row[(o + 4) * 2 + k];
-          lv.G.irow[d][10 + (o + 2) * 2 + k] = n >= 15 ? row[18 + (o + 4) * 2 + k] : 0.f;
+          lv.G.irow[d][10 + (o + 2) * 2 + k] = n >= 15 ? row[kTabKT + (o + 4) * 2 + k] : 0.f;
         }
-      for (int o = -4; o <= 4; ++o) lv.G.irow[d][20 + o + 4] = n >= 15 ? row[36 + o + 5] : 0.f;
+      for (int o = -4; o <= 4; ++o) lv.G.irow[d][20 + o + 4] = n >= 15 ? row[kTabP0 + o + 5] : 0.f;
     }
     launch_schur_coef(lv.G, B, lv.c, lv.cf, s);
     launch_diag_schur(lv.G, B, lv.cf, lv.dinv, s);

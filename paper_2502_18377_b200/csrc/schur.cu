@@ -9,10 +9,10 @@
 //   S x   = sum_d P0_d x - sum_d K_d^T (u~_d h) + sigma alpha h + w_bnd^2 [p in B] x.
 // K_d, K_d^T and P0_d depend only on the index along axis d (13 classes near the edges,
 // constant inside): their rows are tabulated on the host in fp64 (no run-time
-// cancellation of the large h^-k terms) -- 48 floats per (axis, index):
+// cancellation of the large h^-k terms) -- kTabRow = 52 floats per (axis, index):
 //   [0,18)  Kf[o][k]  coefficient of x(i+o) in (K x)_k(i),      o = -4..4
-//   [18,36) KT[o][k]  coefficient of q_k(i+o) in (K^T q)(i),    o = -4..4
-//   [36,47) P0[o]     coefficient of x(i+o) in (P0 x)(i),       o = -5..5
+//   [20,38) KT[o][k]  coefficient of q_k(i+o) in (K^T q)(i),    o = -4..4
+//   [40,51) P0[o]     coefficient of x(i+o) in (P0 x)(i),       o = -5..5
 // Per point the kernels read cf = [sigma alpha, 1/sigma, u~ (2D)] (2+2D floats).
 #include "common.cuh"
 #include "internal.h"
@@ -102,21 +102,21 @@ __device__ __forceinline__ T schur_s_point(const Geo& G, const float* __restrict
     const float* u2 = cf + (size_t)(3 + 2 * d) * P;
     if (i >= 7 && i <= n - 8) {  // P0 reach 4 and K^T reach 2 away from the edge classes
 #pragma unroll
-      for (int o = -4; o <= 4; ++o) acc += T(__ldg(row + 36 + o + 5)) * T(x[p + o * s]);
+      for (int o = -4; o <= 4; ++o) acc += T(__ldg(row + kTabP0 + o + 5)) * T(x[p + o * s]);
 #pragma unroll
       for (int o = -2; o <= 2; ++o) {
         const int q = p + o * s;
-        acc -= (T(__ldg(row + 18 + (o + 4) * 2)) * T(u1[q]) +
-                T(__ldg(row + 18 + (o + 4) * 2 + 1)) * T(u2[q])) * hb[q];
+        acc -= (T(__ldg(row + kTabKT + (o + 4) * 2)) * T(u1[q]) +
+                T(__ldg(row + kTabKT + (o + 4) * 2 + 1)) * T(u2[q])) * hb[q];
       }
     } else {
       const int lo = max(-5, -i), hi = min(5, n - 1 - i);
-      for (int o = lo; o <= hi; ++o) acc += T(__ldg(row + 36 + o + 5)) * T(x[p + o * s]);
+      for (int o = lo; o <= hi; ++o) acc += T(__ldg(row + kTabP0 + o + 5)) * T(x[p + o * s]);
       const int lo2 = max(-4, -i), hi2 = min(4, n - 1 - i);
       for (int o = lo2; o <= hi2; ++o) {
         const int q = p + o * s;
-        acc -= (T(__ldg(row + 18 + (o + 4) * 2)) * T(u1[q]) +
-                T(__ldg(row + 18 + (o + 4) * 2 + 1)) * T(u2[q])) * hb[q];
+        acc -= (T(__ldg(row + kTabKT + (o + 4) * 2)) * T(u1[q]) +
+                T(__ldg(row + kTabKT + (o + 4) * 2 + 1)) * T(u2[q])) * hb[q];
       }
     }
   }
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_diag(Geo G, const float* __r
   for (int d = 0; d < D; ++d) {
     const int n = G.n[d], s = G.stride[d], i = idx[d];
     const float* row = tab_row(G, d, i);
-    diag += row[36 + 5];
+    diag += row[kTabP0 + 5];
     for (int o = max(-4, -i); o <= min(4, n - 1 - i); ++o) {
       const int q = p + o * s;
       double dh;
@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(kThreads) k_schur_diag(Geo G, const float* __r
              double(cb[(size_t)(3 + 2 * d) * P + q]) * rq[(-o + 4) * 2 + 1];
         dh *= double(cb[P + q]);
       }
-      diag -= (double(row[18 + (o + 4) * 2]) * cb[(size_t)(2 + 2 * d) * P + q] +
-               double(row[18 + (o + 4) * 2 + 1]) * cb[(size_t)(3 + 2 * d) * P + q]) * dh;
+      diag -= (double(row[kTabKT + (o + 4) * 2]) * cb[(size_t)(2 + 2 * d) * P + q] +
+               double(row[kTabKT + (o + 4) * 2 + 1]) * cb[(size_t)(3 + 2 * d) * P + q]) * dh;
     }
   }
   dinv[(size_t)v * P + p] = float(1.0 / diag);
@@ -273,11 +273,55 @@ __device__ __forceinline__ void stT4(T* p, const T* v) {
   }
 }
 #define F4(a, j) (j == 0 ? a.x : (j == 1 ? a.y : (j == 2 ? a.z : a.w)))
+// NV 16-byte loads of a table-row segment (rows and segments are 16-byte aligned): one
+// vector load per 4 coefficients instead of one scalar load each (L1 wavefronts)
+template <int NV>
+__device__ __forceinline__ void ldv(const float* p, float* v) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p) + k);
+    v[4 * k] = a.x;
+    v[4 * k + 1] = a.y;
+    v[4 * k + 2] = a.z;
+    v[4 * k + 3] = a.w;
+  }
+}
+
+// Warp-specialised quad mapping along the contiguous axis (NY4 = n_last / 4 a power of two
+// <= kThreads): a CTA covers R = kThreads / NY4 whole rows; its first R * NI threads take the
+// interior quads 2 .. NY4-3 (ymode 1: constant-bank interior stencils, no per-point branch)
+// and the remaining threads the (up to 4) edge quads (ymode 2: table rows for every point),
+// so the edge handling never diverges inside a warp.  ymode 0 = per-point test (no remap).
+__device__ __forceinline__ void remap_quad(int NY4, int& row, int& q, int& ymode) {
+  const int R = kThreads / NY4;
+  const int NE = NY4 < 4 ? NY4 : 4, NI = NY4 - NE;
+  int k = threadIdx.x;
+  if (k < R * NI) {
+    row = k / NI;
+    q = 2 + k % NI;
+    ymode = 1;
+  } else {
+    k -= R * NI;
+    row = k / NE;
+    const int e = k % NE;
+    q = (NE == 4 && e >= 2) ? NY4 - 4 + e : e;
+    ymode = 2;
+  }
+  row += blockIdx.x * R;
+}
+// points handled by this CTA (profiling counters)
+__device__ __forceinline__ int block_points(int remap, int P, int nlast, int p0_first) {
+  if (remap) {
+    const int R = kThreads / (nlast >> 2), rows = P / nlast;
+    return max(0, min(R, rows - (int)blockIdx.x * R)) * nlast;
+  }
+  return min(4 * kThreads, P - p0_first);
+}
 
 template <int D, typename T>
 __device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__ cb,
                                          const float* __restrict__ xb, int p0, const int* idx,
-                                         T* g) {
+                                         T* g, int ymode) {
   const int P = G.P;
   {
     const float4 x0 = ld4(xb + p0), c0 = ld4(cb + p0);
@@ -300,13 +344,14 @@ __device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__
         }
       }
     } else {  // edge rows: unrolled, clamped addresses, zero coefficients out of range
-      const float* row = tab_row(G, d, i);
+      float kf[20];
+      ldv<5>(tab_row(G, d, i) + kTabKf, kf);
       const int olo = -i, ohi = n - 1 - i;
 #pragma unroll
       for (int o = -4; o <= 4; ++o) {
         const int oc = o < olo ? olo : (o > ohi ? ohi : o);
         const float4 xv = ld4(xb + p0 + oc * s);
-        const T a = __ldg(row + (o + 4) * 2), b = __ldg(row + (o + 4) * 2 + 1);
+        const T a = kf[(o + 4) * 2], b = kf[(o + 4) * 2 + 1];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           k1[j] += a * T(F4(xv, j));
@@ -336,19 +381,20 @@ __device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__
     for (int j = 0; j < 4; ++j) {
       const int i = i0 + j;
       T k1 = 0, k2 = 0;
-      if (i >= 2 && i <= n - 3) {
+      if (ymode == 1 || (ymode == 0 && i >= 2 && i <= n - 3)) {
 #pragma unroll
         for (int o = -2; o <= 2; ++o) {
           k1 += T(G.irow[d][(o + 2) * 2]) * T(w[4 + j + o]);
           k2 += T(G.irow[d][(o + 2) * 2 + 1]) * T(w[4 + j + o]);
         }
       } else {
-        const float* row = tab_row(G, d, i);
+        float kf[20];
+        ldv<5>(tab_row(G, d, i) + kTabKf, kf);
 #pragma unroll
         for (int o = -4; o <= 4; ++o) {  // out-of-range taps have zero coefficients
           if (4 + j + o < 0 || 4 + j + o > 11) continue;
-          k1 += T(__ldg(row + (o + 4) * 2)) * T(w[4 + j + o]);
-          k2 += T(__ldg(row + (o + 4) * 2 + 1)) * T(w[4 + j + o]);
+          k1 += T(kf[(o + 4) * 2]) * T(w[4 + j + o]);
+          k2 += T(kf[(o + 4) * 2 + 1]) * T(w[4 + j + o]);
         }
       }
       g[j] -= T(F4(ua, j)) * k1 + T(F4(ub, j)) * k2;
@@ -364,7 +410,7 @@ __device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__
 template <int D, typename T>
 __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__ cb,
                                          const float* __restrict__ xb, const T* __restrict__ hb,
-                                         int p0, const int* idx, T* acc) {
+                                         int p0, const int* idx, T* acc, int ymode) {
   const int P = G.P;
   {
     T h0[4];
@@ -411,12 +457,15 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
       // edge classes: fully unrolled, addresses clamped into the line (the table holds
       // zero coefficients for out-of-range taps) so that every load issues at once
       const float* row = tab_row(G, d, i);
+      float p0r[12], ktr[20];
+      ldv<3>(row + kTabP0, p0r);
+      ldv<5>(row + kTabKT, ktr);
       const int olo = -i, ohi = n - 1 - i;
 #pragma unroll
       for (int o = -5; o <= 5; ++o) {
         const int oc = o < olo ? olo : (o > ohi ? ohi : o);
         const float4 xv = ld4(xb + p0 + oc * s);
-        const T a = __ldg(row + 36 + o + 5);
+        const T a = p0r[o + 5];
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[j] += a * T(F4(xv, j));
       }
@@ -427,7 +476,7 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
         const float4 va = ld4(u1 + q), vb = ld4(u2 + q);
         T hv[4];
         ldT4<T>(hb + q, hv);
-        const T a = __ldg(row + 18 + (o + 4) * 2), b = __ldg(row + 18 + (o + 4) * 2 + 1);
+        const T a = ktr[(o + 4) * 2], b = ktr[(o + 4) * 2 + 1];
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[j] -= (a * T(F4(va, j)) + b * T(F4(vb, j))) * hv[j];
       }
@@ -467,7 +516,7 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int i = i0 + j;
-      if (i >= 7 && i <= n - 8) {
+      if (ymode == 1 || (ymode == 0 && i >= 7 && i <= n - 8)) {
 #pragma unroll
         for (int o = -4; o <= 4; ++o) acc[j] += T(G.irow[d][20 + o + 4]) * T(xw[8 + j + o]);
 #pragma unroll
@@ -476,13 +525,16 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
                      T(G.irow[d][10 + (o + 2) * 2 + 1]) * T(bw[4 + j + o])) * hw[4 + j + o];
       } else {
         const float* row = tab_row(G, d, i);
+        float p0r[12], ktr[20];
+        ldv<3>(row + kTabP0, p0r);
+        ldv<5>(row + kTabKT, ktr);
 #pragma unroll
-        for (int o = -5; o <= 5; ++o) acc[j] += T(__ldg(row + 36 + o + 5)) * T(xw[8 + j + o]);
+        for (int o = -5; o <= 5; ++o) acc[j] += T(p0r[o + 5]) * T(xw[8 + j + o]);
 #pragma unroll
         for (int o = -4; o <= 4; ++o) {
           if (4 + j + o < 0 || 4 + j + o > 11) continue;
-          acc[j] -= (T(__ldg(row + 18 + (o + 4) * 2)) * T(aw[4 + j + o]) +
-                     T(__ldg(row + 18 + (o + 4) * 2 + 1)) * T(bw[4 + j + o])) * hw[4 + j + o];
+          acc[j] -= (T(ktr[(o + 4) * 2]) * T(aw[4 + j + o]) +
+                     T(ktr[(o + 4) * 2 + 1]) * T(bw[4 + j + o])) * hw[4 + j + o];
         }
       }
     }
@@ -493,29 +545,42 @@ template <int D, typename T>
 __global__ void __launch_bounds__(kThreads) k_schur_h_v4(Geo G, const float* __restrict__ cf, int crep,
                                                         const float* __restrict__ x,
                                                         T* __restrict__ hout, const int* act,
-                                                        unsigned long long* pts) {
+                                                        unsigned long long* pts, int remap) {
   constexpr int NC = 2 + 2 * D;
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
-  const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int nl = G.n[D - 1];
+  if (pts && threadIdx.x == 0)
+    atomicAdd(pts, (unsigned long long)block_points(remap, P, nl, blockIdx.x * blockDim.x * 4));
+  int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4, ymode = 0;
+  if (remap) {
+    int row, q;
+    remap_quad(nl >> 2, row, q, ymode);
+    p0 = row * nl + 4 * q;
+  }
   if (p0 >= P) return;
   int idx[D];
   unravel<D>(G, p0, idx);
   T g[4];
-  schur_h4<D, T>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, p0, idx, g);
+  schur_h4<D, T>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, p0, idx, g, ymode);
   stT4<T>(hout + (size_t)v * P + p0, g);
-  if (pts && threadIdx.x == 0) atomicAdd(pts, (unsigned long long)min(4 * kThreads, P - p0));
 }
 
 template <int D, int EPI, typename T>
 __global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const float* __restrict__ cf, int crep,
                                                         const float* __restrict__ x,
                                                         const T* __restrict__ hb, EpiArgs A,
-                                                        const int* act) {
+                                                        const int* act, int remap) {
   constexpr int NC = 2 + 2 * D;
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
-  const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int nl = G.n[D - 1];
+  int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4, ymode = 0;
+  if (remap) {
+    int row, q;
+    remap_quad(nl >> 2, row, q, ymode);
+    p0 = row * nl + 4 * q;
+  }
   double dot = 0.0;
   if (p0 < P) {
     int idx[D];
@@ -523,7 +588,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const float* __r
     const size_t o = (size_t)v * P + p0;
     T acc[4];
     schur_s4<D, T>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, hb + (size_t)v * P, p0, idx,
-                   acc);
+                   acc, ymode);
     float q[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) q[j] = float(acc[j]);
@@ -590,8 +655,9 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const float* __r
       }
     }
   }
-  if (A.pts && threadIdx.x == 0 && p0 < P)
-    atomicAdd(A.pts + EPI, (unsigned long long)min(4 * kThreads, P - p0));
+  if (A.pts && threadIdx.x == 0)
+    atomicAdd(A.pts + EPI,
+              (unsigned long long)block_points(remap, P, nl, blockIdx.x * blockDim.x * 4));
   if (EPI == EPI_DOT || EPI == EPI_POWER ||
       ((EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST || EPI == EPI_POST0) && A.rdot)) {
     dot = block_sum(dot);
@@ -646,27 +712,33 @@ __device__ __forceinline__ void pencil2(const Geo& G, const float* __restrict__ 
   const float* r0 = tab_row(G, AX, i0);
   const float* r1 = tab_row(G, AX, ok1 ? i0 + 1 : i0);
   const float m1 = ok1 ? 1.f : 0.f;
+  float p0a[12], p0b[12];
+  ldv<3>(r0 + kTabP0, p0a);
+  ldv<3>(r1 + kTabP0, p0b);
 #pragma unroll
   for (int u = -5; u <= 6; ++u) {
     const int ic = min(max(i0 + u, 0), n - 1);
     const float4 xv = ld4(xb + pbase + (ic - i0) * s);
-    const float c0 = u <= 5 ? __ldg(r0 + 36 + u + 5) : 0.f;
-    const float c1 = u >= -4 ? m1 * __ldg(r1 + 36 + u - 1 + 5) : 0.f;
+    const float c0 = u <= 5 ? p0a[u + 5] : 0.f;
+    const float c1 = u >= -4 ? m1 * p0b[u - 1 + 5] : 0.f;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       acc0[j] += c0 * F4(xv, j);
       acc1[j] += c1 * F4(xv, j);
     }
   }
+  float kta[20], ktb[20];
+  ldv<5>(r0 + kTabKT, kta);
+  ldv<5>(r1 + kTabKT, ktb);
 #pragma unroll
   for (int u = -4; u <= 5; ++u) {
     const int ic = min(max(i0 + u, 0), n - 1);
     const int q = pbase + (ic - i0) * s;
     const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
-    const float a0 = u <= 4 ? __ldg(r0 + 18 + (u + 4) * 2) : 0.f;
-    const float b0 = u <= 4 ? __ldg(r0 + 18 + (u + 4) * 2 + 1) : 0.f;
-    const float a1 = u >= -3 ? m1 * __ldg(r1 + 18 + (u + 3) * 2) : 0.f;
-    const float b1 = u >= -3 ? m1 * __ldg(r1 + 18 + (u + 3) * 2 + 1) : 0.f;
+    const float a0 = u <= 4 ? kta[(u + 4) * 2] : 0.f;
+    const float b0 = u <= 4 ? kta[(u + 4) * 2 + 1] : 0.f;
+    const float a1 = u >= -3 ? m1 * ktb[(u + 3) * 2] : 0.f;
+    const float b1 = u >= -3 ? m1 * ktb[(u + 3) * 2 + 1] : 0.f;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       acc0[j] -= (a0 * F4(va, j) + b0 * F4(vb, j)) * F4(hv, j);
@@ -702,12 +774,15 @@ __device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ 
     return;
   }
   const float* row = tab_row(G, AX, i);
+  float p0r[12], ktr[20];
+  ldv<3>(row + kTabP0, p0r);
+  ldv<5>(row + kTabKT, ktr);
   const int olo = -i, ohi = n - 1 - i;
 #pragma unroll
   for (int o = -5; o <= 5; ++o) {
     const int oc = o < olo ? olo : (o > ohi ? ohi : o);
     const float4 xv = ld4(xb + p0 + oc * s);
-    const float a = __ldg(row + 36 + o + 5);
+    const float a = p0r[o + 5];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] += a * F4(xv, j);
   }
@@ -716,7 +791,7 @@ __device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ 
     const int oc = o < olo ? olo : (o > ohi ? ohi : o);
     const int q = p0 + oc * s;
     const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
-    const float a = __ldg(row + 18 + (o + 4) * 2), b = __ldg(row + 18 + (o + 4) * 2 + 1);
+    const float a = ktr[(o + 4) * 2], b = ktr[(o + 4) * 2 + 1];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] -= (a * F4(va, j) + b * F4(vb, j)) * F4(hv, j);
   }
@@ -726,7 +801,7 @@ __device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ 
 __device__ __forceinline__ void quad_y_own(const Geo& G, const float* __restrict__ cb,
                                            const float* __restrict__ xb,
                                            const float* __restrict__ hb, int p0, int t, int xr,
-                                           float* acc) {
+                                           float* acc, int ymode) {
   const int P = G.P, n = G.n[2], i0 = p0 % n;
   {
     const float4 h0 = ld4(hb + p0), c0 = ld4(cb + p0), x0 = ld4(xb + p0);
@@ -766,7 +841,7 @@ __device__ __forceinline__ void quad_y_own(const Geo& G, const float* __restrict
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int i = i0 + j;
-    if (i >= 7 && i <= n - 8) {
+    if (ymode == 1 || (ymode == 0 && i >= 7 && i <= n - 8)) {
 #pragma unroll
       for (int o = -4; o <= 4; ++o) acc[j] += G.irow[2][20 + o + 4] * xw[8 + j + o];
 #pragma unroll
@@ -775,13 +850,16 @@ __device__ __forceinline__ void quad_y_own(const Geo& G, const float* __restrict
                    G.irow[2][10 + (o + 2) * 2 + 1] * bw[4 + j + o]) * hw[4 + j + o];
     } else {
       const float* row = tab_row(G, 2, i);
+      float p0r[12], ktr[20];
+      ldv<3>(row + kTabP0, p0r);
+      ldv<5>(row + kTabKT, ktr);
 #pragma unroll
-      for (int o = -5; o <= 5; ++o) acc[j] += __ldg(row + 36 + o + 5) * xw[8 + j + o];
+      for (int o = -5; o <= 5; ++o) acc[j] += p0r[o + 5] * xw[8 + j + o];
 #pragma unroll
       for (int o = -4; o <= 4; ++o) {
         if (4 + j + o < 0 || 4 + j + o > 11) continue;
-        acc[j] -= (__ldg(row + 18 + (o + 4) * 2) * aw[4 + j + o] +
-                   __ldg(row + 18 + (o + 4) * 2 + 1) * bw[4 + j + o]) * hw[4 + j + o];
+        acc[j] -= (ktr[(o + 4) * 2] * aw[4 + j + o] +
+                   ktr[(o + 4) * 2 + 1] * bw[4 + j + o]) * hw[4 + j + o];
       }
     }
   }
@@ -860,14 +938,16 @@ template <int EPI, int BX>
 __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __restrict__ cf, int crep,
                                                          const float* __restrict__ x,
                                                          const float* __restrict__ hb, EpiArgs A,
-                                                         const int* act) {
+                                                         const int* act, int remap) {
   // BX = 1: 2x2 blocking in (t, x); BX = 0: 2x1 blocking in t only (fewer registers)
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
   const int nt = G.n[0], nx = G.n[1], ny = G.n[2];
   const int NY4 = ny >> 2, NXB = BX ? (nx + 1) >> 1 : nx, NT2 = (nt + 1) >> 1;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int yq = tid % NY4, r2 = tid / NY4, xp = r2 % NXB, tp = r2 / NXB;
+  int yq = tid % NY4, r2 = tid / NY4, ymode = 0;
+  if (remap) remap_quad(NY4, r2, yq, ymode);
+  const int xp = r2 % NXB, tp = r2 / NXB;
   double dot = 0.0;
   int nq = 0;
   if (tp < NT2) {
@@ -901,7 +981,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __
       for (int b = 0; b < BX + 1; ++b) {
         if ((a && !okt) || (b && !okx)) continue;
         const int p0 = pb + a * st + b * sxs;
-        quad_y_own(G, cb, xb, hv, p0, t0 + a, x0 + b, acc[a][b]);
+        quad_y_own(G, cb, xb, hv, p0, t0 + a, x0 + b, acc[a][b], ymode);
         dot += quad_epilogue<EPI>(A, pde, (size_t)v * P + p0, x, acc[a][b]);
         ++nq;
       }
@@ -941,6 +1021,11 @@ void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStrea
 }
 
 static inline bool use_v4(const Geo& G) { return (G.n[G.D - 1] & 3) == 0; }
+// warp-specialised interior / edge quads (remap_quad): NY4 a power of two dividing kThreads
+static inline int use_remap(const Geo& G) {
+  const int q = G.n[G.D - 1] >> 2;
+  return use_v4(G) && q > 0 && (q & (q - 1)) == 0 && q <= kThreads;
+}
 // 2x2 (t,x)-blocked pass 2: 3D, fp32, n_y % 4 == 0
 static int g_block_mode = -1;  // 0: v4, 1: 2x1 (t), 2: 2x2 (t,x); env MPDE_SCHUR_BLOCK
 static inline int block_mode() {
@@ -968,9 +1053,9 @@ void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const flo
   if (use_v4(G)) {
     dim3 gr((G.P + 4 * kThreads - 1) / (4 * kThreads), nvec);
     if (f64)
-      DISPATCH_D2(G.D, k_schur_h_v4<DD, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (double*)g, act, pts));
+      DISPATCH_D2(G.D, k_schur_h_v4<DD, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (double*)g, act, pts, 0));
     else
-      DISPATCH_D2(G.D, k_schur_h_v4<DD, float><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (float*)g, act, pts));
+      DISPATCH_D2(G.D, k_schur_h_v4<DD, float><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (float*)g, act, pts, 0));
     return;
   }
   if (f64)
@@ -984,12 +1069,13 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
   ++g_launch_count;
   if (use_b22(G, f64)) {
     const dim3 gb(schur_tiles(G, f64), nvec);
+    const int rm = use_remap(G);
 #define B22_CASE(E)                                                                          \
   case E:                                                                                    \
     if (block_mode() == 2)                                                                   \
-      k_schur_s_b22<E, 1><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act);  \
+      k_schur_s_b22<E, 1><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm);  \
     else                                                                                     \
-      k_schur_s_b22<E, 0><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act);  \
+      k_schur_s_b22<E, 0><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm);  \
     break;
     switch (epi) {
       B22_CASE(EPI_STORE)
@@ -1004,14 +1090,15 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
     return;
   }
   const bool v4 = use_v4(G);
+  const int rm = use_remap(G);
   dim3 gr(schur_tiles(G, f64), nvec);
 #define EPI_CASE2(E)                                                                              \
   case E:                                                                                         \
     if (v4) {                                                                                     \
       if (f64)                                                                                    \
-        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const double*)g, A, act)); \
+        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const double*)g, A, act, rm)); \
       else                                                                                        \
-        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, float><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act)); \
+        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, float><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm)); \
     } else if (f64)                                                                               \
       DISPATCH_D2(G.D, k_schur_s<DD, E, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const double*)g, A, act)); \
     else                                                                                          \
