@@ -100,6 +100,10 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* c,
 void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStream_t s);
 // number of CTAs (= partial sums per vector) of the S kernels on this level
 int schur_tiles(const Geo& G, bool f64);
+// true when this level applies S with the single fused kernel (launch_schur_fused)
+bool schur_fused(const Geo& G, bool f64);
+void launch_schur_fused(int epi, const Geo& G, int nvec, int crep, const float* cf,
+                        const float* x, const EpiArgs& A, const int* act, cudaStream_t s);
 void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaStream_t s);
 void launch_restrict(const Geo& Gf, const Geo& Gc, int nvec, int nfield, const float* fine,
                      float* coarse, const int* act, int crep, cudaStream_t s);

@@ -448,6 +448,11 @@ int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const flo
   Level& lv = h->lv[l];
   EpiArgs A2 = A;
   A2.pts = g_prof.on ? g_prof.d_pts : nullptr;
+  if (schur_fused(lv.G, f64)) {
+    PROF(1, s, launch_schur_fused(epi, lv.G, nvec, crep, lv.cf, x, A2, act, s));
+    CKL();
+    return MPDE_OK;
+  }
   PROF(0, s, launch_schur_g(lv.G, nvec, crep, lv.cf, x, lv.g, act, A2.pts ? A2.pts + 8 : nullptr,
                             f64, s));
   PROF(1, s, launch_schur_out(epi, lv.G, nvec, crep, lv.cf, x, lv.g, A2, act, f64, s));

@@ -1001,6 +1001,351 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Fused S apply for 3D fp32 levels: both passes in one kernel, all neighbour data from
+// shared memory.  One CTA per (vector, tile of kFX x-rows x all y), marching along t:
+//   step j:  x plane j+5 -> smem ring (cp.async, one plane ahead of use)
+//            h(j), Q_d = u~_d h(j) on the tile rows + 2 halo rows (x from the smem ring,
+//            cf from HBM), Q_x / Q_y -> smem (this plane only)
+//            t-direction terms of S are SCATTERED: x(j) and Q_t(j) add
+//              P0_i[j-i] x(j) - KT_i[j-i] . Q_t(j)   to the accumulators of planes
+//            i = j-5 .. j+5 (a thread-private smem ring), plus sigma alpha h(j) to plane j
+//            x / y terms of plane j (gathered from the smem plane) -> accumulator j
+//            plane j-5 is complete -> epilogue (the same EpiArgs contract as pass 2)
+// HBM traffic per point: x 4 + cf 32 + the epilogue's vectors (no h round trip, cf read
+// once instead of twice).  The t-direction coefficient rows of step j (uniform over the
+// CTA) are staged in smem by the first threads.
+// ---------------------------------------------------------------------------------
+constexpr int kFX = 8;     // x rows per tile
+constexpr int kFXR = 10;   // x-plane ring: planes j-4 .. j+5
+constexpr int kFAR = 11;   // accumulator ring: planes j-5 .. j+5
+constexpr int kFLag = 5;   // plane j - kFLag is output at step j
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void sts4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void f4axpy(float4& a, float c, float4 x) {
+  a.x += c * x.x;
+  a.y += c * x.y;
+  a.z += c * x.z;
+  a.w += c * x.w;
+}
+
+static inline size_t fused_smem_floats(int n2) {
+  return (size_t)kFXR * (kFX + 8) * n2 + (size_t)4 * (kFX + 4) * n2 + (size_t)kFAR * kFX * n2 + 64;
+}
+
+template <int EPI>
+__global__ void k_schur_fused(Geo G, const float* __restrict__ cf, int crep,
+                              const float* __restrict__ x, EpiArgs A, const int* act) {
+  extern __shared__ __align__(16) float fsm[];
+  const int v = blockIdx.y, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  const int n0 = G.n[0], n1 = G.n[1], n2 = G.n[2], s0 = G.stride[0];
+  const int NY4 = n2 >> 2, X0 = blockIdx.x * kFX;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int hr = tid / NY4, q = tid - hr * NY4, y0 = 4 * q;
+  const int xg = X0 - 2 + hr;                       // this thread's h row
+  const bool hval = xg >= 0 && xg < n1;
+  const bool own = hr >= 2 && hr < kFX + 2;         // tile row -> owns an output quad
+  const int orow = hr - 2;
+  float* xs = fsm;                                   // [kFXR][kFX+8][n2]
+  float* qs = xs + (size_t)kFXR * (kFX + 8) * n2;    // [4][kFX+4][n2]
+  float* as = qs + (size_t)4 * (kFX + 4) * n2;       // [kFAR][kFX][n2]
+  float* ct = as + (size_t)kFAR * kFX * n2;          // [18] Kf_t(j), [33] scatter rows
+  const int xrow_sz = (kFX + 8) * n2, qrow_sz = (kFX + 4) * n2, arow_sz = kFX * n2;
+  const float* cb = cf + (size_t)pde * 8 * P;
+  const float* xb = x + (size_t)v * P;
+  const float wb2 = G.wb * G.wb;
+
+  auto load_plane = [&](int k) {
+    if (k < n0) {
+      float* dst = xs + (k % kFXR) * xrow_sz;
+      const float* src = xb + (size_t)k * s0;
+      for (int c = tid; c < (kFX + 8) * NY4; c += nthr) {
+        const int r = c / NY4, qq = c - r * NY4, xr = X0 - 4 + r;
+        if (xr >= 0 && xr < n1) cp_async16(dst + r * n2 + 4 * qq, src + (size_t)xr * n2 + 4 * qq);
+      }
+    }
+    cp_async_commit();
+  };
+  if (own)
+    for (int m = 0; m < kFAR; ++m) sts4(as + m * arow_sz + orow * n2 + y0, make_float4(0.f, 0.f, 0.f, 0.f));
+#pragma unroll 1
+  for (int k = 0; k < kFLag; ++k) load_plane(k);
+
+  double dot = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < n0 + kFLag; ++j) {
+    if (j < n0) {
+      load_plane(j + kFLag);
+      // t-direction coefficient rows of this step (uniform): Kf row j, scatter rows i=j-5..j+5
+      if (tid < 18) {
+        const int o = tid / 2 - 4, k = tid & 1;
+        ct[tid] = (j + o >= 0 && j + o < n0) ? __ldg(tab_row(G, 0, j) + kTabKf + (o + 4) * 2 + k) : 0.f;
+      } else if (tid < 51) {
+        const int m = (tid - 18) / 3, c = (tid - 18) % 3, i = j - kFLag + m, o = j - i;
+        float val = 0.f;
+        if (i >= 0 && i < n0) {
+          const float* row = tab_row(G, 0, i);
+          if (c == 0) val = __ldg(row + kTabP0 + o + 5);
+          else if (o >= -4 && o <= 4) val = __ldg(row + kTabKT + (o + 4) * 2 + (c - 1));
+        }
+        ct[tid] = val;
+      }
+      cp_async_wait1();
+      __syncthreads();
+      const float* xj = xs + (j % kFXR) * xrow_sz;  // plane j
+      // ---- h(j), Q on the h rows --------------------------------------------------------
+      float4 qx1 = make_float4(0.f, 0.f, 0.f, 0.f), qx2 = qx1, qy1 = qx1, qy2 = qx1;
+      if (hval) {
+        const size_t pg = (size_t)j * s0 + (size_t)xg * n2 + y0;
+        const float4 csa = ld4(cb + pg), cis = ld4(cb + P + pg);
+        const float4 ut1 = ld4(cb + 2 * (size_t)P + pg), ut2 = ld4(cb + 3 * (size_t)P + pg);
+        const float4 ux1 = ld4(cb + 4 * (size_t)P + pg), ux2 = ld4(cb + 5 * (size_t)P + pg);
+        const float4 uy1 = ld4(cb + 6 * (size_t)P + pg), uy2 = ld4(cb + 7 * (size_t)P + pg);
+        const int xrr = hr + 2;  // row of xg in the x ring
+        const float4 x0 = lds4(xj + xrr * n2 + y0);
+        float g[4] = {csa.x * x0.x, csa.y * x0.y, csa.z * x0.z, csa.w * x0.w};
+        {  // t
+          float4 k1 = make_float4(0.f, 0.f, 0.f, 0.f), k2 = k1;
+          if (j >= 2 && j <= n0 - 3) {
+#pragma unroll
+            for (int o = -2; o <= 2; ++o) {
+              const float4 xv = lds4(xs + ((j + o) % kFXR) * xrow_sz + xrr * n2 + y0);
+              f4axpy(k1, G.irow[0][(o + 2) * 2], xv);
+              f4axpy(k2, G.irow[0][(o + 2) * 2 + 1], xv);
+            }
+          } else {
+#pragma unroll
+            for (int o = -4; o <= 4; ++o) {
+              const int pc = min(max(j + o, 0), n0 - 1);
+              const float4 xv = lds4(xs + (pc % kFXR) * xrow_sz + xrr * n2 + y0);
+              f4axpy(k1, ct[(o + 4) * 2], xv);
+              f4axpy(k2, ct[(o + 4) * 2 + 1], xv);
+            }
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) g[jj] -= F4(ut1, jj) * F4(k1, jj) + F4(ut2, jj) * F4(k2, jj);
+        }
+        {  // x
+          float4 k1 = make_float4(0.f, 0.f, 0.f, 0.f), k2 = k1;
+          if (xg >= 2 && xg <= n1 - 3) {
+#pragma unroll
+            for (int o = -2; o <= 2; ++o) {
+              const float4 xv = lds4(xj + (xrr + o) * n2 + y0);
+              f4axpy(k1, G.irow[1][(o + 2) * 2], xv);
+              f4axpy(k2, G.irow[1][(o + 2) * 2 + 1], xv);
+            }
+          } else {
+            float kf[20];
+            ldv<5>(tab_row(G, 1, xg) + kTabKf, kf);
+#pragma unroll
+            for (int o = -4; o <= 4; ++o) {
+              const int oc = min(max(xg + o, 0), n1 - 1) - xg;
+              const float4 xv = lds4(xj + (xrr + oc) * n2 + y0);
+              f4axpy(k1, kf[(o + 4) * 2], xv);
+              f4axpy(k2, kf[(o + 4) * 2 + 1], xv);
+            }
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) g[jj] -= F4(ux1, jj) * F4(k1, jj) + F4(ux2, jj) * F4(k2, jj);
+        }
+        {  // y: window x(y0-4 .. y0+7) of this row
+          const float* xr = xj + xrr * n2;
+          float w[12];
+          const float4 wl = y0 >= 4 ? lds4(xr + y0 - 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 wr = y0 + 4 < n2 ? lds4(xr + y0 + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            w[jj] = F4(wl, jj);
+            w[4 + jj] = F4(x0, jj);
+            w[8 + jj] = F4(wr, jj);
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int i = y0 + jj;
+            float k1 = 0.f, k2 = 0.f;
+            if (i >= 2 && i <= n2 - 3) {
+#pragma unroll
+              for (int o = -2; o <= 2; ++o) {
+                k1 += G.irow[2][(o + 2) * 2] * w[4 + jj + o];
+                k2 += G.irow[2][(o + 2) * 2 + 1] * w[4 + jj + o];
+              }
+            } else {
+              float kf[20];
+              ldv<5>(tab_row(G, 2, i) + kTabKf, kf);
+#pragma unroll
+              for (int o = -4; o <= 4; ++o) {
+                if (4 + jj + o < 0 || 4 + jj + o > 11) continue;
+                k1 += kf[(o + 4) * 2] * w[4 + jj + o];
+                k2 += kf[(o + 4) * 2 + 1] * w[4 + jj + o];
+              }
+            }
+            g[jj] -= F4(uy1, jj) * k1 + F4(uy2, jj) * k2;
+          }
+        }
+        float4 hq;
+        hq.x = F4(cis, 0) * g[0];
+        hq.y = F4(cis, 1) * g[1];
+        hq.z = F4(cis, 2) * g[2];
+        hq.w = F4(cis, 3) * g[3];
+        qx1 = make_float4(ux1.x * hq.x, ux1.y * hq.y, ux1.z * hq.z, ux1.w * hq.w);
+        qx2 = make_float4(ux2.x * hq.x, ux2.y * hq.y, ux2.z * hq.z, ux2.w * hq.w);
+        qy1 = make_float4(uy1.x * hq.x, uy1.y * hq.y, uy1.z * hq.z, uy1.w * hq.w);
+        qy2 = make_float4(uy2.x * hq.x, uy2.y * hq.y, uy2.z * hq.z, uy2.w * hq.w);
+        if (own) {  // scatter the t terms of x(j), Q_t(j) and sigma alpha h(j)
+          const float4 qt1 = make_float4(ut1.x * hq.x, ut1.y * hq.y, ut1.z * hq.z, ut1.w * hq.w);
+          const float4 qt2 = make_float4(ut2.x * hq.x, ut2.y * hq.y, ut2.z * hq.z, ut2.w * hq.w);
+          float* ab = as + orow * n2 + y0;
+#pragma unroll
+          for (int m = 0; m < 2 * kFLag + 1; ++m) {
+            const int i = j - kFLag + m;
+            const float cp = ct[18 + 3 * m], ck1 = ct[19 + 3 * m], ck2 = ct[20 + 3 * m];
+            if (i < 0 || i >= n0 || (cp == 0.f && ck1 == 0.f && ck2 == 0.f && m != kFLag)) continue;
+            float* a = ab + (i % kFAR) * arow_sz;
+            float4 av = lds4(a);
+            f4axpy(av, cp, x0);
+            f4axpy(av, -ck1, qt1);
+            f4axpy(av, -ck2, qt2);
+            if (m == kFLag) {
+              av.x += csa.x * hq.x;
+              av.y += csa.y * hq.y;
+              av.z += csa.z * hq.z;
+              av.w += csa.w * hq.w;
+            }
+            sts4(a, av);
+          }
+        }
+      }
+      sts4(qs + 0 * qrow_sz + hr * n2 + y0, qx1);
+      sts4(qs + 1 * qrow_sz + hr * n2 + y0, qx2);
+      sts4(qs + 2 * qrow_sz + hr * n2 + y0, qy1);
+      sts4(qs + 3 * qrow_sz + hr * n2 + y0, qy2);
+      __syncthreads();
+      // ---- x / y terms of plane j on the tile rows ----------------------------------------
+      if (own) {
+        const int xo = X0 + orow, xrr = orow + 4, qrr = orow + 2;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (xo >= 7 && xo <= n1 - 8) {
+#pragma unroll
+          for (int o = -4; o <= 4; ++o) f4axpy(acc, G.irow[1][20 + o + 4], lds4(xj + (xrr + o) * n2 + y0));
+#pragma unroll
+          for (int o = -2; o <= 2; ++o) {
+            f4axpy(acc, -G.irow[1][10 + (o + 2) * 2], lds4(qs + (qrr + o) * n2 + y0));
+            f4axpy(acc, -G.irow[1][10 + (o + 2) * 2 + 1], lds4(qs + qrow_sz + (qrr + o) * n2 + y0));
+          }
+        } else {
+          const float* row = tab_row(G, 1, xo);
+          float p0r[12], ktr[20];
+          ldv<3>(row + kTabP0, p0r);
+          ldv<5>(row + kTabKT, ktr);
+#pragma unroll
+          for (int o = -5; o <= 5; ++o) {
+            const int oc = min(max(xo + o, 0), n1 - 1) - xo;
+            f4axpy(acc, p0r[o + 5], lds4(xj + (xrr + oc) * n2 + y0));
+          }
+#pragma unroll
+          for (int o = -4; o <= 4; ++o) {
+            const int oc = min(max(xo + o, 0), n1 - 1) - xo;
+            const int qr = min(max(qrr + oc, 0), kFX + 3);  // beyond the reach: zero coefficient
+            f4axpy(acc, -ktr[(o + 4) * 2], lds4(qs + qr * n2 + y0));
+            f4axpy(acc, -ktr[(o + 4) * 2 + 1], lds4(qs + qrow_sz + qr * n2 + y0));
+          }
+        }
+        {  // y terms: x window (y0-8 .. y0+11), Q_y windows (y0-4 .. y0+7)
+          const float* xr = xj + xrr * n2;
+          const float* q1 = qs + 2 * qrow_sz + qrr * n2;
+          const float* q2 = qs + 3 * qrow_sz + qrr * n2;
+          float xw[20], aw[12], bw[12];
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const int off = -8 + 4 * k;
+            const bool ok = (y0 + off >= 0) && (y0 + off < n2);
+            const float4 vv = ok ? lds4(xr + y0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) xw[4 * k + jj] = F4(vv, jj);
+          }
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const int off = -4 + 4 * k;
+            const bool ok = (y0 + off >= 0) && (y0 + off < n2);
+            const float4 va = ok ? lds4(q1 + y0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 vb = ok ? lds4(q2 + y0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              aw[4 * k + jj] = F4(va, jj);
+              bw[4 * k + jj] = F4(vb, jj);
+            }
+          }
+          float ay[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int i = y0 + jj;
+            if (i >= 7 && i <= n2 - 8) {
+#pragma unroll
+              for (int o = -4; o <= 4; ++o) ay[jj] += G.irow[2][20 + o + 4] * xw[8 + jj + o];
+#pragma unroll
+              for (int o = -2; o <= 2; ++o)
+                ay[jj] -= G.irow[2][10 + (o + 2) * 2] * aw[4 + jj + o] +
+                          G.irow[2][10 + (o + 2) * 2 + 1] * bw[4 + jj + o];
+            } else {
+              const float* row = tab_row(G, 2, i);
+              float p0r[12], ktr[20];
+              ldv<3>(row + kTabP0, p0r);
+              ldv<5>(row + kTabKT, ktr);
+#pragma unroll
+              for (int o = -5; o <= 5; ++o) ay[jj] += p0r[o + 5] * xw[8 + jj + o];
+#pragma unroll
+              for (int o = -4; o <= 4; ++o) {
+                if (4 + jj + o < 0 || 4 + jj + o > 11) continue;
+                ay[jj] -= ktr[(o + 4) * 2] * aw[4 + jj + o] + ktr[(o + 4) * 2 + 1] * bw[4 + jj + o];
+              }
+            }
+          }
+          const bool face = (j == 0) | (j == n0 - 1) | (xo == 0) | (xo == n1 - 1);
+          const float4 x0 = lds4(xr + y0);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            if (face || y0 + jj == 0 || y0 + jj == n2 - 1) ay[jj] += wb2 * F4(x0, jj);
+          acc.x += ay[0];
+          acc.y += ay[1];
+          acc.z += ay[2];
+          acc.w += ay[3];
+        }
+        float* a = as + (j % kFAR) * arow_sz + orow * n2 + y0;
+        float4 av = lds4(a);
+        av.x += acc.x;
+        av.y += acc.y;
+        av.z += acc.z;
+        av.w += acc.w;
+        sts4(a, av);
+      }
+    }
+    // ---- plane j - kFLag is complete: epilogue ----------------------------------------------
+    if (own && j >= kFLag) {
+      const int i = j - kFLag;
+      float* a = as + (i % kFAR) * arow_sz + orow * n2 + y0;
+      const float4 av = lds4(a);
+      sts4(a, make_float4(0.f, 0.f, 0.f, 0.f));
+      const float qv[4] = {av.x, av.y, av.z, av.w};
+      dot += quad_epilogue<EPI>(A, pde, (size_t)v * P + (size_t)i * s0 + (size_t)(X0 + orow) * n2 + y0, x, qv);
+    }
+    if (j < n0) __syncthreads();
+  }
+  if (A.pts && tid == 0) atomicAdd(A.pts + EPI, (unsigned long long)kFX * n2 * n0);
+  if (EPI == EPI_DOT || EPI == EPI_POWER ||
+      ((EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST || EPI == EPI_POST0) && A.rdot)) {
+    dot = block_sum(dot);
+    if (tid == 0) A.part[(size_t)v * gridDim.x + blockIdx.x] = dot;
+  }
+}
+
 // ------------------------------------------------------------------------- launchers
 static inline dim3 grid2(int P, int nvec) { return dim3((P + kThreads - 1) / kThreads, nvec); }
 
@@ -1042,7 +1387,20 @@ static inline int b22_threads(const Geo& G) {
   const int bx = block_mode() == 2;
   return ((G.n[0] + 1) / 2) * (bx ? (G.n[1] + 1) / 2 : G.n[1]) * (G.n[2] / 4);
 }
+// fused single-kernel S apply (k_schur_fused): 3D fp32 levels with full-row tiles
+static int g_fused = -1;  // env MPDE_FUSED=1 enables (default off: slower)
+static inline bool use_fused(const Geo& G, bool f64) {
+  if (g_fused < 0) {
+    const char* e = getenv("MPDE_FUSED");
+    g_fused = e ? atoi(e) : 0;
+  }
+  const int n1 = G.D == 3 ? G.n[1] : 0, n2 = G.D == 3 ? G.n[2] : 0;
+  return g_fused && G.D == 3 && !f64 && n2 % 4 == 0 && n2 >= 32 && n2 <= 128 &&
+         n1 % kFX == 0 && n1 >= 2 * kFX;
+}
+bool schur_fused(const Geo& G, bool f64) { return use_fused(G, f64); }
 int schur_tiles(const Geo& G, bool f64) {
+  if (use_fused(G, f64)) return G.n[1] / kFX;
   if (use_b22(G, f64)) return (b22_threads(G) + kThreads - 1) / kThreads;
   return use_v4(G) ? (G.P + 4 * kThreads - 1) / (4 * kThreads) : (G.P + kThreads - 1) / kThreads;
 }
@@ -1114,6 +1472,34 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
     EPI_CASE2(EPI_POST0)
   }
 #undef EPI_CASE2
+}
+
+void launch_schur_fused(int epi, const Geo& G, int nvec, int crep, const float* cf,
+                        const float* x, const EpiArgs& A, const int* act, cudaStream_t s) {
+  ++g_launch_count;
+  const dim3 gr(G.n[1] / kFX, nvec);
+  const int thr = (kFX + 4) * (G.n[2] / 4);
+  const size_t smem = sizeof(float) * fused_smem_floats(G.n[2]);
+#define FUSED_CASE(E)                                                                          \
+  case E: {                                                                                    \
+    static size_t attr = 0;                                                                    \
+    if (smem > attr) {                                                                         \
+      cudaFuncSetAttribute(k_schur_fused<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                           (int)smem);                                                         \
+      attr = smem;                                                                             \
+    }                                                                                          \
+    k_schur_fused<E><<<gr, thr, smem, s>>>(G, cf, crep, x, A, act);                            \
+  } break;
+  switch (epi) {
+    FUSED_CASE(EPI_STORE)
+    FUSED_CASE(EPI_DOT)
+    FUSED_CASE(EPI_POWER)
+    FUSED_CASE(EPI_RESID)
+    FUSED_CASE(EPI_SMOOTH)
+    FUSED_CASE(EPI_SMOOTH_LAST)
+    FUSED_CASE(EPI_POST0)
+  }
+#undef FUSED_CASE
 }
 
 void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaStream_t s) {

@@ -1,6 +1,6 @@
 """GPU unit tests of the condensed operator paths at sizes that select each kernel variant
-(scalar, 4-points-per-thread, 2x2-blocked) against the dense Schur complement built from the
-oracle's A, and symmetry / positivity of the V-cycle preconditioner."""
+(scalar, 4-points-per-thread, 2x2-blocked, fused single-kernel) against the Schur complement
+built from the oracle's A, and symmetry / positivity of the V-cycle preconditioner."""
 import numpy as np
 import pytest
 import torch
@@ -41,6 +41,40 @@ def test_schur_variants_match_dense(shape, h):
     for i in range(B):
         S = _dense_schur(pr, c[i].astype(np.float64))
         ref = S @ x[i]
+        assert np.linalg.norm(y[i].cpu().numpy() - ref) <= 1e-4 * np.linalg.norm(ref)
+    s.close()
+
+
+def _sparse_schur_apply(pr, c, x):
+    """S x = N_pp x - N_pd N_dd^-1 N_dp x with sparse N = A^T A (N_dd block-diagonal)."""
+    import scipy.sparse.linalg as sla
+    A, _, _ = assemble(pr, c, np.zeros(pr.P), np.zeros(pr.P))
+    N = (A.T @ A).tocsc()
+    P = pr.P
+    Npp, Npd, Ndp, Ndd = N[:P, :P], N[:P, P:], N[P:, :P], N[P:, P:]
+    return Npp @ x - Npd @ sla.splu(Ndd.tocsc()).solve(Ndp @ x)
+
+
+@pytest.mark.parametrize("shape,h", [((7, 16, 32), (0.05, 0.06, 0.07)),   # fused, 2 x-tiles
+                                     ((9, 24, 36), (0.04, 0.03, 0.05))])  # fused, interior tile
+def test_fused_schur_matches_sparse(shape, h):
+    """The fused single-kernel S apply (3D fp32, n_x % 8 == 0, n_y >= 32) against S applied
+    through the oracle's sparse A (no dense N at these sizes)."""
+    from paper_2502_18377_b200 import mpde
+    rng = np.random.default_rng(7)
+    M, P, B = 7, int(np.prod(shape)), 2
+    c = rng.normal(0.0, 0.5, (B, M, P))
+    c[:, 1] += 1.0
+    c = c.astype(np.float32)
+    w = (1.25, 2.0, 0.75, 0.875)
+    s = mpde.Solver(shape, h, torch.from_numpy(c).cuda(), weights=w)
+    x = rng.normal(size=(B, P)).astype(np.float32)
+    y = torch.empty((B, P), dtype=torch.float32, device="cuda")
+    mpde.mpde_apply_schur(s.h_, 0, torch.from_numpy(x).cuda(), y)
+    torch.cuda.synchronize()
+    pr = Problem(shape, h, *w)
+    for i in range(B):
+        ref = _sparse_schur_apply(pr, c[i].astype(np.float64), x[i].astype(np.float64))
         assert np.linalg.norm(y[i].cpu().numpy() - ref) <= 1e-4 * np.linalg.norm(ref)
     s.close()
 
