@@ -55,28 +55,48 @@ def _sparse_schur_apply(pr, c, x):
     return Npp @ x - Npd @ sla.splu(Ndd.tocsc()).solve(Ndp @ x)
 
 
-@pytest.mark.parametrize("shape,h", [((7, 16, 32), (0.05, 0.06, 0.07)),   # fused, 2 x-tiles
-                                     ((9, 24, 36), (0.04, 0.03, 0.05))])  # fused, interior tile
-def test_fused_schur_matches_sparse(shape, h):
-    """The fused single-kernel S apply (3D fp32, n_x % 8 == 0, n_y >= 32) against S applied
-    through the oracle's sparse A (no dense N at these sizes)."""
-    from paper_2502_18377_b200 import mpde
+_APPLY_SCRIPT = r"""
+import sys, numpy as np, torch
+from paper_2502_18377_b200 import mpde
+d = np.load(sys.argv[1])
+shape, h, w = tuple(int(v) for v in d["shape"]), tuple(d["h"]), tuple(d["w"])
+s = mpde.Solver(shape, h, torch.from_numpy(d["c"]).cuda(), weights=w)
+y = torch.empty(d["x"].shape, dtype=torch.float32, device="cuda")
+mpde.mpde_apply_schur(s.h_, 0, torch.from_numpy(d["x"]).cuda(), y)
+torch.cuda.synchronize()
+np.save(sys.argv[2], y.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("shape,h,fused", [
+    ((7, 16, 32), (0.05, 0.06, 0.07), "1"),   # fused, 2 x-tiles
+    ((9, 24, 36), (0.04, 0.03, 0.05), "1"),   # fused, interior tile
+    ((7, 16, 64), (0.05, 0.06, 0.07), "0"),   # t-blocked pass 2, warp-specialised y quads (NY4=16)
+    ((8, 10, 32), (0.05, 0.06, 0.07), "0")])  # t-blocked pass 2, NY4=8 (4 interior / 4 edge)
+def test_large_schur_matches_sparse(shape, h, fused, tmp_path):
+    """S apply at n_y >= 32 (the warp-specialised and the fused single-kernel paths; the kernel
+    selection MPDE_FUSED is read once per process, so the apply runs in a child process)
+    against S applied through the oracle's sparse A (no dense N at these sizes)."""
+    import os
+    import subprocess
+    import sys
     rng = np.random.default_rng(7)
     M, P, B = 7, int(np.prod(shape)), 2
     c = rng.normal(0.0, 0.5, (B, M, P))
     c[:, 1] += 1.0
     c = c.astype(np.float32)
     w = (1.25, 2.0, 0.75, 0.875)
-    s = mpde.Solver(shape, h, torch.from_numpy(c).cuda(), weights=w)
     x = rng.normal(size=(B, P)).astype(np.float32)
-    y = torch.empty((B, P), dtype=torch.float32, device="cuda")
-    mpde.mpde_apply_schur(s.h_, 0, torch.from_numpy(x).cuda(), y)
-    torch.cuda.synchronize()
+    np.savez(tmp_path / "in.npz", shape=np.array(shape), h=np.array(h), w=np.array(w), c=c, x=x)
+    env = dict(os.environ, MPDE_FUSED=fused)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", _APPLY_SCRIPT, str(tmp_path / "in.npz"),
+                    str(tmp_path / "y.npy")], check=True, env=env, cwd=root)
+    y = np.load(tmp_path / "y.npy")
     pr = Problem(shape, h, *w)
     for i in range(B):
         ref = _sparse_schur_apply(pr, c[i].astype(np.float64), x[i].astype(np.float64))
-        assert np.linalg.norm(y[i].cpu().numpy() - ref) <= 1e-4 * np.linalg.norm(ref)
-    s.close()
+        assert np.linalg.norm(y[i] - ref) <= 1e-4 * np.linalg.norm(ref)
 
 
 @pytest.mark.parametrize("shape,h", [((16, 18, 20), (0.05, 0.06, 0.07)), ((20, 24), (0.05, 0.04))])
