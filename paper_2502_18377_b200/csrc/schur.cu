@@ -670,12 +670,22 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const float* __r
 // (t0+a, x0+b), a, b in {0,1}.  Every t- (x-) neighbour load feeds both t (x) outputs,
 // which cuts the L1 gathers per quad by ~30% (the v4 kernel is L1-wavefront bound).
 // ---------------------------------------------------------------------------------
-template <int AX>  // accumulate the AX-axis (0 = t, 1 = x) terms of a 2-output pencil
+// compile-time (x, y) extents (0 = read from G): every stencil offset becomes an immediate
+template <int NX, int NY>
+__device__ __forceinline__ int dim_n(const Geo& G, int ax) {
+  return ax == 0 ? G.n[0] : ax == 1 ? (NX ? NX : G.n[1]) : (NY ? NY : G.n[2]);
+}
+template <int NX, int NY>
+__device__ __forceinline__ int dim_s(const Geo& G, int ax) {
+  return ax == 0 ? ((NX && NY) ? NX * NY : G.stride[0]) : ax == 1 ? (NY ? NY : G.stride[1]) : 1;
+}
+
+template <int AX, int NX, int NY>  // accumulate the AX-axis (0 = t, 1 = x) terms of a 2-output pencil
 __device__ __forceinline__ void pencil2(const Geo& G, const float* __restrict__ cb,
                                         const float* __restrict__ xb, const float* __restrict__ hb,
                                         int pbase, int i0, bool ok1, float* acc0, float* acc1) {
   // pbase: offset of output 0 (index i0 along AX); output 1 is at pbase + s (index i0+1)
-  const int P = G.P, n = G.n[AX], s = G.stride[AX];
+  const int P = G.P, n = dim_n<NX, NY>(G, AX), s = dim_s<NX, NY>(G, AX);
   const float* u1 = cb + (size_t)(2 + 2 * AX) * P;
   const float* u2 = cb + (size_t)(3 + 2 * AX) * P;
   if (i0 >= 7 && i0 + 1 <= n - 8) {
@@ -748,11 +758,11 @@ __device__ __forceinline__ void pencil2(const Geo& G, const float* __restrict__ 
 }
 
 // one-output version of pencil2 (single quad, AX-axis terms)
-template <int AX>
+template <int AX, int NX, int NY>
 __device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ cb,
                                         const float* __restrict__ xb, const float* __restrict__ hb,
                                         int p0, int i, float* acc) {
-  const int P = G.P, n = G.n[AX], s = G.stride[AX];
+  const int P = G.P, n = dim_n<NX, NY>(G, AX), s = dim_s<NX, NY>(G, AX);
   const float* u1 = cb + (size_t)(2 + 2 * AX) * P;
   const float* u2 = cb + (size_t)(3 + 2 * AX) * P;
   if (i >= 7 && i <= n - 8) {
@@ -798,14 +808,15 @@ __device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ 
 }
 
 // y-axis (contiguous) terms + own terms of one quad, as in schur_s4
+template <int NX, int NY>
 __device__ __forceinline__ void quad_y_own(const Geo& G, const float* __restrict__ cb,
                                            const float* __restrict__ xb,
                                            const float* __restrict__ hb, int p0, int t, int xr,
                                            float* acc, int ymode) {
-  const int P = G.P, n = G.n[2], i0 = p0 % n;
+  const int P = G.P, n = dim_n<NX, NY>(G, 2), i0 = p0 % n;
   {
     const float4 h0 = ld4(hb + p0), c0 = ld4(cb + p0), x0 = ld4(xb + p0);
-    const bool face = (t == 0) | (t == G.n[0] - 1) | (xr == 0) | (xr == G.n[1] - 1);
+    const bool face = (t == 0) | (t == G.n[0] - 1) | (xr == 0) | (xr == dim_n<NX, NY>(G, 1) - 1);
     const float wb2 = G.wb * G.wb;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -934,7 +945,7 @@ __device__ __forceinline__ double quad_epilogue(const EpiArgs& A, int pde, size_
   return dot;
 }
 
-template <int EPI, int BX>
+template <int EPI, int BX, int NX, int NY>
 __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __restrict__ cf, int crep,
                                                          const float* __restrict__ x,
                                                          const float* __restrict__ hb, EpiArgs A,
@@ -942,7 +953,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __
   // BX = 1: 2x2 blocking in (t, x); BX = 0: 2x1 blocking in t only (fewer registers)
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
-  const int nt = G.n[0], nx = G.n[1], ny = G.n[2];
+  const int nt = G.n[0], nx = dim_n<NX, NY>(G, 1), ny = dim_n<NX, NY>(G, 2);
   const int NY4 = ny >> 2, NXB = BX ? (nx + 1) >> 1 : nx, NT2 = (nt + 1) >> 1;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int yq = tid % NY4, r2 = tid / NY4, ymode = 0;
@@ -956,7 +967,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __
     const float* hv = hb + (size_t)v * P;
     const int t0 = 2 * tp, x0 = BX ? 2 * xp : xp;
     const bool okt = t0 + 1 < nt, okx = BX && (x0 + 1 < nx);
-    const int st = G.stride[0], sxs = G.stride[1];
+    const int st = dim_s<NX, NY>(G, 0), sxs = dim_s<NX, NY>(G, 1);
     const int pb = t0 * st + x0 * sxs + 4 * yq;
     float acc[2][BX + 1][4];
 #pragma unroll
@@ -966,14 +977,14 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[a][b][j] = 0.f;
     // t pencils (columns x0 [, x0+1]) and x terms (planes t0, t0+1)
-    pencil2<0>(G, cb, xb, hv, pb, t0, okt, acc[0][0], acc[1][0]);
+    pencil2<0, NX, NY>(G, cb, xb, hv, pb, t0, okt, acc[0][0], acc[1][0]);
     if (BX) {
-      if (okx) pencil2<0>(G, cb, xb, hv, pb + sxs, t0, okt, acc[0][BX], acc[1][BX]);
-      pencil2<1>(G, cb, xb, hv, pb, x0, okx, acc[0][0], acc[0][BX]);
-      if (okt) pencil2<1>(G, cb, xb, hv, pb + st, x0, okx, acc[1][0], acc[1][BX]);
+      if (okx) pencil2<0, NX, NY>(G, cb, xb, hv, pb + sxs, t0, okt, acc[0][BX], acc[1][BX]);
+      pencil2<1, NX, NY>(G, cb, xb, hv, pb, x0, okx, acc[0][0], acc[0][BX]);
+      if (okt) pencil2<1, NX, NY>(G, cb, xb, hv, pb + st, x0, okx, acc[1][0], acc[1][BX]);
     } else {
-      pencil1<1>(G, cb, xb, hv, pb, x0, acc[0][0]);
-      if (okt) pencil1<1>(G, cb, xb, hv, pb + st, x0, acc[1][0]);
+      pencil1<1, NX, NY>(G, cb, xb, hv, pb, x0, acc[0][0]);
+      if (okt) pencil1<1, NX, NY>(G, cb, xb, hv, pb + st, x0, acc[1][0]);
     }
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -981,7 +992,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __
       for (int b = 0; b < BX + 1; ++b) {
         if ((a && !okt) || (b && !okx)) continue;
         const int p0 = pb + a * st + b * sxs;
-        quad_y_own(G, cb, xb, hv, p0, t0 + a, x0 + b, acc[a][b], ymode);
+        quad_y_own<NX, NY>(G, cb, xb, hv, p0, t0 + a, x0 + b, acc[a][b], ymode);
         dot += quad_epilogue<EPI>(A, pde, (size_t)v * P + p0, x, acc[a][b]);
         ++nq;
       }
@@ -1346,6 +1357,247 @@ __global__ void k_schur_fused(Geo G, const float* __restrict__ cf, int crep,
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Pass 2, shared-memory tiled (3D fp32, n_y = NY in {32, 64, 128}): a CTA computes a tile of
+// kTT t-planes x kTX x-rows x all y.  Every operand it reads with a halo is staged once in
+// shared memory with cp.async (axis-aligned cross halos only: the t column of the tile's
+// rows, the x rows of the tile's planes), then each thread evaluates one y-quad from smem
+// (no per-tap global address arithmetic, L1-latency operands).  Regions (rows of NY floats):
+//   XA x  planes t0-5 .. t0+kTT+4, tile rows        XC x  tile planes, rows X0-5 .. X0+kTX+4
+//   HA h  planes t0-4 .. t0+kTT+3, tile rows        HC h  tile planes, rows X0-4 .. X0+kTX+3
+//   UT u~_t (2) like HA   UX u~_x (2) like HC   UY u~_y (2), SA sigma alpha: tile planes/rows
+// (halos = the largest reach of the edge-class rows: P0 5 (rows 0 <-> 5), K^T 4)
+// Out-of-domain rows are zero-filled; their coefficients are zero.
+// ---------------------------------------------------------------------------------
+constexpr int kTT = 4, kTX = 4;
+constexpr int kTPL = kTT + 8;            // planes in the t-column regions of h, u~_t
+constexpr int kTPX = kTT + 10;           // planes in the t-column region of x
+constexpr int kTRows = kTPX * kTX /*XA*/ + kTT * (kTX + 10) /*XC*/ + kTPL * kTX /*HA*/ +
+                       kTT * (kTX + 8) /*HC*/ + 2 * kTPL * kTX /*UT*/ + 2 * kTT * (kTX + 8) /*UX*/ +
+                       2 * kTT * kTX /*UY*/ + kTT * kTX /*SA*/;
+static inline size_t tile_smem_bytes(int ny) { return sizeof(float) * (size_t)kTRows * ny; }
+
+template <int EPI, int NY>
+__global__ void __launch_bounds__(4 * NY) k_schur_s_tile(Geo G, const float* __restrict__ cf, int crep,
+                                                        const float* __restrict__ x,
+                                                        const float* __restrict__ hb, EpiArgs A,
+                                                        const int* act) {
+  constexpr int NQ = NY / 4, NTH = 4 * NY;  // threads = kTT * kTX * NQ
+  extern __shared__ __align__(16) float tsm[];
+  const int v = blockIdx.y, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  const int n0 = G.n[0], n1 = G.n[1];
+  const int s0 = n1 * NY;
+  const int nxt = n1 / kTX;
+  const int X0 = (blockIdx.x % nxt) * kTX, t0 = (blockIdx.x / nxt) * kTT;
+  float* XA = tsm;
+  float* XC = XA + kTPX * kTX * NY;
+  float* HA = XC + kTT * (kTX + 10) * NY;
+  float* HC = HA + kTPL * kTX * NY;
+  float* UT = HC + kTT * (kTX + 8) * NY;
+  float* UX = UT + 2 * kTPL * kTX * NY;
+  float* UY = UX + 2 * kTT * (kTX + 8) * NY;
+  float* SA = UY + 2 * kTT * kTX * NY;
+  const float* cb = cf + (size_t)pde * 8 * P;
+  const float* xb = x + (size_t)v * P;
+  const float* hv = hb + (size_t)v * P;
+  const int tid = threadIdx.x;
+  // ---- stage: one 16-byte chunk per (row, quad); rows outside the domain -> zeros --------
+  auto stage = [&](float* dst, const float* src, int pl0, int npl, int r0, int nr) {
+    const int n = npl * nr * NQ;
+    for (int c = tid; c < n; c += NTH) {
+      const int qq = c % NQ, rr = c / NQ, r = rr % nr, pl = rr / nr;
+      const int t = pl0 + pl, xr = r0 + r;
+      float* d = dst + (size_t)rr * NY + 4 * qq;
+      if (t >= 0 && t < n0 && xr >= 0 && xr < n1)
+        cp_async16(d, src + (size_t)t * s0 + (size_t)xr * NY + 4 * qq);
+      else
+        *reinterpret_cast<float4*>(d) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  stage(XA, xb, t0 - 5, kTPX, X0, kTX);
+  stage(XC, xb, t0, kTT, X0 - 5, kTX + 10);
+  stage(HA, hv, t0 - 4, kTPL, X0, kTX);
+  stage(HC, hv, t0, kTT, X0 - 4, kTX + 8);
+  stage(UT, cb + 2 * (size_t)P, t0 - 4, kTPL, X0, kTX);
+  stage(UT + kTPL * kTX * NY, cb + 3 * (size_t)P, t0 - 4, kTPL, X0, kTX);
+  stage(UX, cb + 4 * (size_t)P, t0, kTT, X0 - 4, kTX + 8);
+  stage(UX + kTT * (kTX + 8) * NY, cb + 5 * (size_t)P, t0, kTT, X0 - 4, kTX + 8);
+  stage(UY, cb + 6 * (size_t)P, t0, kTT, X0, kTX);
+  stage(UY + kTT * kTX * NY, cb + 7 * (size_t)P, t0, kTT, X0, kTX);
+  stage(SA, cb, t0, kTT, X0, kTX);
+  cp_async_commit();
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+
+  // ---- this thread's quad: warp-specialised interior / edge y quads over 16 tile rows ------
+  constexpr int NE = NQ < 4 ? NQ : 4, NI = NQ - NE, R = kTT * kTX;
+  int rr, q, ymode;
+  if (tid < R * NI) {
+    rr = tid / NI;
+    q = 2 + tid % NI;
+    ymode = 1;
+  } else {
+    const int k = tid - R * NI, e = k % NE;
+    rr = k / NE;
+    q = (NE == 4 && e >= 2) ? NQ - 4 + e : e;
+    ymode = 2;
+  }
+  const int tt = rr / kTX, xx = rr % kTX, t = t0 + tt, xo = X0 + xx, y0 = 4 * q;
+  double dot = 0.0;
+  if (t < n0) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const float* xa = XA + xx * NY + y0;             // + plane * kTX * NY
+    const float* ha = HA + xx * NY + y0;
+    const float* u1a = UT + xx * NY + y0;
+    const float* u2a = u1a + kTPL * kTX * NY;
+    const int pa = tt + 4, px = tt + 5;              // this plane in the t-column regions
+    // t terms
+    if (t >= 7 && t <= n0 - 8) {
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        const float4 xv = lds4(xa + (px + o) * kTX * NY);
+        const float c = G.irow[0][20 + o + 4];
+        acc[0] += c * xv.x; acc[1] += c * xv.y; acc[2] += c * xv.z; acc[3] += c * xv.w;
+      }
+#pragma unroll
+      for (int o = -2; o <= 2; ++o) {
+        const int off = (pa + o) * kTX * NY;
+        const float4 va = lds4(u1a + off), vb = lds4(u2a + off), hq = lds4(ha + off);
+        const float a = G.irow[0][10 + (o + 2) * 2], b = G.irow[0][10 + (o + 2) * 2 + 1];
+        acc[0] -= (a * va.x + b * vb.x) * hq.x; acc[1] -= (a * va.y + b * vb.y) * hq.y;
+        acc[2] -= (a * va.z + b * vb.z) * hq.z; acc[3] -= (a * va.w + b * vb.w) * hq.w;
+      }
+    } else {
+      const float* row = tab_row(G, 0, t);
+      float p0r[12], ktr[20];
+      ldv<3>(row + kTabP0, p0r);
+      ldv<5>(row + kTabKT, ktr);
+#pragma unroll
+      for (int o = -5; o <= 5; ++o) {
+        const float4 xv = lds4(xa + (px + o) * kTX * NY);
+        const float c = p0r[o + 5];
+        acc[0] += c * xv.x; acc[1] += c * xv.y; acc[2] += c * xv.z; acc[3] += c * xv.w;
+      }
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        const int off = (pa + o) * kTX * NY;
+        const float4 va = lds4(u1a + off), vb = lds4(u2a + off), hq = lds4(ha + off);
+        const float a = ktr[(o + 4) * 2], b = ktr[(o + 4) * 2 + 1];
+        acc[0] -= (a * va.x + b * vb.x) * hq.x; acc[1] -= (a * va.y + b * vb.y) * hq.y;
+        acc[2] -= (a * va.z + b * vb.z) * hq.z; acc[3] -= (a * va.w + b * vb.w) * hq.w;
+      }
+    }
+    // x terms
+    const float* xc = XC + (tt * (kTX + 10) + xx + 5) * NY + y0;
+    const float* hc = HC + (tt * (kTX + 8) + xx + 4) * NY + y0;
+    const float* u1c = UX + (tt * (kTX + 8) + xx + 4) * NY + y0;
+    const float* u2c = u1c + kTT * (kTX + 8) * NY;
+    if (xo >= 7 && xo <= n1 - 8) {
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        const float4 xv = lds4(xc + o * NY);
+        const float c = G.irow[1][20 + o + 4];
+        acc[0] += c * xv.x; acc[1] += c * xv.y; acc[2] += c * xv.z; acc[3] += c * xv.w;
+      }
+#pragma unroll
+      for (int o = -2; o <= 2; ++o) {
+        const float4 va = lds4(u1c + o * NY), vb = lds4(u2c + o * NY), hq = lds4(hc + o * NY);
+        const float a = G.irow[1][10 + (o + 2) * 2], b = G.irow[1][10 + (o + 2) * 2 + 1];
+        acc[0] -= (a * va.x + b * vb.x) * hq.x; acc[1] -= (a * va.y + b * vb.y) * hq.y;
+        acc[2] -= (a * va.z + b * vb.z) * hq.z; acc[3] -= (a * va.w + b * vb.w) * hq.w;
+      }
+    } else {
+      const float* row = tab_row(G, 1, xo);
+      float p0r[12], ktr[20];
+      ldv<3>(row + kTabP0, p0r);
+      ldv<5>(row + kTabKT, ktr);
+#pragma unroll
+      for (int o = -5; o <= 5; ++o) {
+        const float4 xv = lds4(xc + o * NY);
+        const float c = p0r[o + 5];
+        acc[0] += c * xv.x; acc[1] += c * xv.y; acc[2] += c * xv.z; acc[3] += c * xv.w;
+      }
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        const float4 va = lds4(u1c + o * NY), vb = lds4(u2c + o * NY), hq = lds4(hc + o * NY);
+        const float a = ktr[(o + 4) * 2], b = ktr[(o + 4) * 2 + 1];
+        acc[0] -= (a * va.x + b * vb.x) * hq.x; acc[1] -= (a * va.y + b * vb.y) * hq.y;
+        acc[2] -= (a * va.z + b * vb.z) * hq.z; acc[3] -= (a * va.w + b * vb.w) * hq.w;
+      }
+    }
+    // y terms and own terms
+    {
+      const float* u1y = UY + (tt * kTX + xx) * NY;
+      const float* u2y = u1y + kTT * kTX * NY;
+      const float* xr = xc - y0;
+      const float* hr = hc - y0;
+      float xw[20], aw[12], bw[12], hw[12];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int off = y0 - 8 + 4 * k;
+        const bool ok = ymode == 1 || (off >= 0 && off < NY);
+        const float4 vv = ok ? lds4(xr + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+        xw[4 * k] = vv.x; xw[4 * k + 1] = vv.y; xw[4 * k + 2] = vv.z; xw[4 * k + 3] = vv.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int off = y0 - 4 + 4 * k;
+        const bool ok = ymode == 1 || (off >= 0 && off < NY);
+        const float4 va = ok ? lds4(u1y + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 vb = ok ? lds4(u2y + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 hq = ok ? lds4(hr + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+        aw[4 * k] = va.x; aw[4 * k + 1] = va.y; aw[4 * k + 2] = va.z; aw[4 * k + 3] = va.w;
+        bw[4 * k] = vb.x; bw[4 * k + 1] = vb.y; bw[4 * k + 2] = vb.z; bw[4 * k + 3] = vb.w;
+        hw[4 * k] = hq.x; hw[4 * k + 1] = hq.y; hw[4 * k + 2] = hq.z; hw[4 * k + 3] = hq.w;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (ymode == 1) {
+#pragma unroll
+          for (int o = -4; o <= 4; ++o) acc[j] += G.irow[2][20 + o + 4] * xw[8 + j + o];
+#pragma unroll
+          for (int o = -2; o <= 2; ++o)
+            acc[j] -= (G.irow[2][10 + (o + 2) * 2] * aw[4 + j + o] +
+                       G.irow[2][10 + (o + 2) * 2 + 1] * bw[4 + j + o]) * hw[4 + j + o];
+        } else {
+          const float* row = tab_row(G, 2, y0 + j);
+          float p0r[12], ktr[20];
+          ldv<3>(row + kTabP0, p0r);
+          ldv<5>(row + kTabKT, ktr);
+#pragma unroll
+          for (int o = -5; o <= 5; ++o) acc[j] += p0r[o + 5] * xw[8 + j + o];
+#pragma unroll
+          for (int o = -4; o <= 4; ++o) {
+            if (4 + j + o < 0 || 4 + j + o > 11) continue;
+            acc[j] -= (ktr[(o + 4) * 2] * aw[4 + j + o] + ktr[(o + 4) * 2 + 1] * bw[4 + j + o]) *
+                      hw[4 + j + o];
+          }
+        }
+      }
+      const float4 sa = lds4(SA + (tt * kTX + xx) * NY + y0);
+      const bool face = (t == 0) | (t == n0 - 1) | (xo == 0) | (xo == n1 - 1);
+      const float wb2 = G.wb * G.wb;
+      const float sav[4] = {sa.x, sa.y, sa.z, sa.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[j] += sav[j] * hw[4 + j];
+        if (face || y0 + j == 0 || y0 + j == NY - 1) acc[j] += wb2 * xw[8 + j];
+      }
+    }
+    dot = quad_epilogue<EPI>(A, pde, (size_t)v * P + (size_t)t * s0 + (size_t)xo * NY + y0, x, acc);
+  }
+  if (A.pts && tid == 0) {
+    const int nt = min(kTT, n0 - t0);
+    atomicAdd(A.pts + EPI, (unsigned long long)nt * kTX * NY);
+  }
+  if (EPI == EPI_DOT || EPI == EPI_POWER ||
+      ((EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST || EPI == EPI_POST0) && A.rdot)) {
+    dot = block_sum(dot);
+    if (tid == 0) A.part[(size_t)v * gridDim.x + blockIdx.x] = dot;
+  }
+}
+
 // ------------------------------------------------------------------------- launchers
 static inline dim3 grid2(int P, int nvec) { return dim3((P + kThreads - 1) / kThreads, nvec); }
 
@@ -1399,8 +1651,21 @@ static inline bool use_fused(const Geo& G, bool f64) {
          n1 % kFX == 0 && n1 >= 2 * kFX;
 }
 bool schur_fused(const Geo& G, bool f64) { return use_fused(G, f64); }
+// smem-tiled pass 2 (k_schur_s_tile): 3D fp32, n_y in {32, 64, 128}, n_x % kTX == 0
+static int g_tile = -1;  // env MPDE_TILE=1 enables (default off: slower)
+static inline bool use_tile(const Geo& G, bool f64) {
+  if (g_tile < 0) {
+    const char* e = getenv("MPDE_TILE");
+    g_tile = e ? atoi(e) : 0;
+  }
+  if (!g_tile || G.D != 3 || f64) return false;
+  const int n2 = G.n[2];
+  return (n2 == 32 || n2 == 64 || n2 == 128) && G.n[1] % kTX == 0 && G.n[1] >= 2 * kTX;
+}
+static inline int tile_ctas(const Geo& G) { return ((G.n[0] + kTT - 1) / kTT) * (G.n[1] / kTX); }
 int schur_tiles(const Geo& G, bool f64) {
   if (use_fused(G, f64)) return G.n[1] / kFX;
+  if (use_tile(G, f64)) return tile_ctas(G);
   if (use_b22(G, f64)) return (b22_threads(G) + kThreads - 1) / kThreads;
   return use_v4(G) ? (G.P + 4 * kThreads - 1) / (4 * kThreads) : (G.P + kThreads - 1) / kThreads;
 }
@@ -1425,15 +1690,57 @@ void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const flo
 void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf, const float* x,
                       const void* g, const EpiArgs& A, const int* act, bool f64, cudaStream_t s) {
   ++g_launch_count;
+  if (use_tile(G, f64)) {
+    const dim3 gt(tile_ctas(G), nvec);
+    const size_t smem = tile_smem_bytes(G.n[2]);
+#define TILE_LAUNCH(E, NYv)                                                                  \
+  {                                                                                          \
+    static bool attr = false;                                                                \
+    if (!attr) {                                                                             \
+      cudaFuncSetAttribute(k_schur_s_tile<E, NYv>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)tile_smem_bytes(NYv));                                       \
+      attr = true;                                                                           \
+    }                                                                                        \
+    k_schur_s_tile<E, NYv><<<gt, 4 * NYv, smem, s>>>(G, cf, crep, x, (const float*)g, A, act); \
+  }
+#define TILE_CASE(E)                                                                         \
+  case E:                                                                                    \
+    if (G.n[2] == 64) TILE_LAUNCH(E, 64)                                                     \
+    else if (G.n[2] == 32) TILE_LAUNCH(E, 32)                                                \
+    else TILE_LAUNCH(E, 128)                                                                 \
+    break;
+    switch (epi) {
+      TILE_CASE(EPI_STORE)
+      TILE_CASE(EPI_DOT)
+      TILE_CASE(EPI_POWER)
+      TILE_CASE(EPI_RESID)
+      TILE_CASE(EPI_SMOOTH)
+      TILE_CASE(EPI_SMOOTH_LAST)
+      TILE_CASE(EPI_POST0)
+    }
+#undef TILE_CASE
+#undef TILE_LAUNCH
+    return;
+  }
   if (use_b22(G, f64)) {
     const dim3 gb(schur_tiles(G, f64), nvec);
     const int rm = use_remap(G);
+#define B22_LAUNCH(E, BXv)                                                                   \
+  if (G.n[1] == 64 && G.n[2] == 64)                                                          \
+    k_schur_s_b22<E, BXv, 64, 64><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
+  else if (G.n[1] == 32 && G.n[2] == 32)                                                     \
+    k_schur_s_b22<E, BXv, 32, 32><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
+  else if (G.n[1] == 128 && G.n[2] == 128)                                                   \
+    k_schur_s_b22<E, BXv, 128, 128><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
+  else                                                                                       \
+    k_schur_s_b22<E, BXv, 0, 0><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm);
 #define B22_CASE(E)                                                                          \
   case E:                                                                                    \
-    if (block_mode() == 2)                                                                   \
-      k_schur_s_b22<E, 1><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm);  \
-    else                                                                                     \
-      k_schur_s_b22<E, 0><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm);  \
+    if (block_mode() == 2) {                                                                 \
+      B22_LAUNCH(E, 1)                                                                       \
+    } else {                                                                                 \
+      B22_LAUNCH(E, 0)                                                                       \
+    }                                                                                        \
     break;
     switch (epi) {
       B22_CASE(EPI_STORE)
@@ -1445,6 +1752,7 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
       B22_CASE(EPI_POST0)
     }
 #undef B22_CASE
+#undef B22_LAUNCH
     return;
   }
   const bool v4 = use_v4(G);

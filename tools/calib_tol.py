@@ -14,14 +14,14 @@ from paper_2502_18377_b200 import mpde  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 B = 4
-settings = [dict(), dict(tol_z=1e-4), dict(tol_z=1e-6), dict(tol_inner=1e-3),
-            dict(tol_inner=1e-4), dict(tol_inner=3e-3)]
+settings = [dict(), dict(tol_inner=1e-3), dict(tol_inner=3e-3), dict(tol_inner=1e-2),
+            dict(tol_inner=3e-2), dict(tol_inner=1e-2, tol_z=1e-5)]
 bt = synth.make_batch(name, batch=B)
 g = synth.make_g(name, batch=B)
 mm = synth.make_mms(name, batch=B)
 cfg = bt["cfg"]
 ref = gu.gpu_solve(cfg.shape, cfg.h, bt["c"], bt["b"], bt["omega"], g,
-                   opts=mpde.mpde_default_options(tol=1e-11, max_refine=12, tol_inner=1e-5))
+                   opts=mpde.mpde_default_options(tol=1e-11, max_refine=12, tol_inner=1e-5, tol_z=1e-9))
 for kw in settings:
     o = mpde.mpde_default_options(**kw)
     out = gu.gpu_solve(cfg.shape, cfg.h, bt["c"], bt["b"], bt["omega"], g, opts=o)
