@@ -958,7 +958,14 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int yq = tid % NY4, r2 = tid / NY4, ymode = 0;
   if (remap) remap_quad(NY4, r2, yq, ymode);
-  const int xp = r2 % NXB, tp = r2 / NXB;
+  int xp = r2 % NXB, tp = r2 / NXB;
+  if (remap > 1) {  // CTA = TPB t-pairs x XPB x-rows (t-neighbour reuse in L1), TPB = remap
+    const int R = kThreads / NY4, TPB = remap, XPB = R / TPB, nxb = (NXB + XPB - 1) / XPB;
+    const int lr = r2 - (int)blockIdx.x * R, bx = blockIdx.x % nxb, bt = blockIdx.x / nxb;
+    xp = bx * XPB + lr % XPB;
+    tp = bt * TPB + lr / XPB;
+    if (xp >= NXB) tp = NT2;  // outside: skip
+  }
   double dot = 0.0;
   int nq = 0;
   if (tp < NT2) {
@@ -1639,6 +1646,24 @@ static inline int b22_threads(const Geo& G) {
   const int bx = block_mode() == 2;
   return ((G.n[0] + 1) / 2) * (bx ? (G.n[1] + 1) / 2 : G.n[1]) * (G.n[2] / 4);
 }
+// t-pairs per CTA of the t-blocked pass 2 (env MPDE_B22_TP, default 1 = one x-row strip;
+// 2/4/8 measured 3-10% slower at C4)
+static int g_b22_tp = -1;
+static inline int b22_tp(const Geo& G) {
+  if (g_b22_tp < 0) {
+    const char* e = getenv("MPDE_B22_TP");
+    g_b22_tp = e ? atoi(e) : 1;
+  }
+  const int R = kThreads / (G.n[2] / 4);
+  if (!use_remap(G) || block_mode() != 1 || g_b22_tp <= 1 || R % g_b22_tp) return 1;
+  return g_b22_tp;
+}
+static inline int b22_ctas(const Geo& G) {
+  const int tp = b22_tp(G);
+  if (tp <= 1) return (b22_threads(G) + kThreads - 1) / kThreads;
+  const int R = kThreads / (G.n[2] / 4), XPB = R / tp;
+  return ((G.n[0] + 1) / 2 + tp - 1) / tp * ((G.n[1] + XPB - 1) / XPB);
+}
 // fused single-kernel S apply (k_schur_fused): 3D fp32 levels with full-row tiles
 static int g_fused = -1;  // env MPDE_FUSED=1 enables (default off: slower)
 static inline bool use_fused(const Geo& G, bool f64) {
@@ -1666,7 +1691,7 @@ static inline int tile_ctas(const Geo& G) { return ((G.n[0] + kTT - 1) / kTT) * 
 int schur_tiles(const Geo& G, bool f64) {
   if (use_fused(G, f64)) return G.n[1] / kFX;
   if (use_tile(G, f64)) return tile_ctas(G);
-  if (use_b22(G, f64)) return (b22_threads(G) + kThreads - 1) / kThreads;
+  if (use_b22(G, f64)) return b22_ctas(G);
   return use_v4(G) ? (G.P + 4 * kThreads - 1) / (4 * kThreads) : (G.P + kThreads - 1) / kThreads;
 }
 
@@ -1724,7 +1749,7 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
   }
   if (use_b22(G, f64)) {
     const dim3 gb(schur_tiles(G, f64), nvec);
-    const int rm = use_remap(G);
+    const int rm = use_remap(G) ? b22_tp(G) : 0;  // >1: t-pair tiling (remap implied)
 #define B22_LAUNCH(E, BXv)                                                                   \
   if (G.n[1] == 64 && G.n[2] == 64)                                                          \
     k_schur_s_b22<E, BXv, 64, 64><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
