@@ -308,9 +308,141 @@ __global__ void __launch_bounds__(256) k_prolong1(Geo Gf, Geo Gc, const float* _
   fine[(size_t)v * Pf + p] = acc;
 }
 
+// Quad versions (4 consecutive points of the last axis per thread, float4 stores): the
+// weights of the non-last axes are computed once per quad and the last-axis taps come from
+// a small window with static offsets (same arithmetic as the scalar kernels above).
+template <int D>
+__global__ void __launch_bounds__(256) k_restrict1q(Geo Gf, Geo Gc, const float* __restrict__ fine,
+                                                   float* __restrict__ coarse, const int* act) {
+  const int v = blockIdx.y, Pc = Gc.P, Pf = Gf.P;
+  if (act && !act[v]) return;
+  const int I0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (I0 >= Pc) return;
+  int cidx[D];
+  unravel<D>(Gc, I0, cidx);
+  constexpr int L = D - 1;
+  const int nfy = Gf.n[L], ncy = Gc.n[L], Yq = cidx[L];  // Yq = 4 * quad index
+  int f[D - 1][4];
+  float w[D - 1][4];
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) restrict_axis(cidx[d], Gf.n[d], Gc.n[d], f[d], w[d]);
+  float wy[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int fj[4];
+    restrict_axis(Yq + j, nfy, ncy, fj, wy[j]);
+  }
+  const float* fb = fine + (size_t)v * Pf;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const bool ycoarse = nfy != ncy;
+  const int ylo = 2 * Yq - 4;  // window fine y ylo .. ylo+15 (coarsened y)
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    if (w[0][a] == 0.f) continue;
+#pragma unroll
+    for (int b = 0; b < (D == 3 ? 4 : 1); ++b) {
+      float wab = w[0][a];
+      const float* row = fb + (size_t)f[0][a] * Gf.stride[0];
+      if (D == 3) {
+        if (w[D - 2][b] == 0.f) continue;
+        wab *= w[D - 2][b];
+        row += (size_t)f[D - 2][b] * Gf.stride[D - 2];
+      }
+      if (ycoarse) {
+        float win[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int y = ylo + 4 * k;
+          const float4 t = (y >= 0 && y < nfy) ? *reinterpret_cast<const float4*>(row + y)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+          win[4 * k] = t.x; win[4 * k + 1] = t.y; win[4 * k + 2] = t.z; win[4 * k + 3] = t.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // fine 2(Yq+j)-1+c = ylo + 2j + 3 + c
+          float sy = 0.f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) sy += wy[j][c] * win[2 * j + 3 + c];
+          acc[j] += wab * sy;
+        }
+      } else {
+        const float4 t = *reinterpret_cast<const float4*>(row + Yq);
+        acc[0] += wab * t.x; acc[1] += wab * t.y; acc[2] += wab * t.z; acc[3] += wab * t.w;
+      }
+    }
+  }
+  *reinterpret_cast<float4*>(coarse + (size_t)v * Pc + I0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_prolong1q(Geo Gf, Geo Gc, const float* __restrict__ coarse,
+                                                  float* __restrict__ fine, const int* act) {
+  const int v = blockIdx.y, Pf = Gf.P, Pc = Gc.P;
+  if (act && !act[v]) return;
+  const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (p0 >= Pf) return;
+  int idx[D];
+  unravel<D>(Gf, p0, idx);
+  constexpr int L = D - 1;
+  const int nfy = Gf.n[L], ncy = Gc.n[L], y0 = idx[L];
+  int I0[D - 1], I1[D - 1];
+  float w0[D - 1], w1[D - 1];
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) prolong_axis(idx[d], Gf.n[d], Gc.n[d], I0[d], I1[d], w0[d], w1[d]);
+  const float* cb = coarse + (size_t)v * Pc;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int q2 = y0 >> 1;  // 2q
+#pragma unroll
+  for (int mask = 0; mask < (1 << (D - 1)); ++mask) {
+    float w = 1.f;
+    int off = 0;
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d) {
+      const bool hi = (mask >> d) & 1;
+      w *= hi ? w1[d] : w0[d];
+      off += (hi ? I1[d] : I0[d]) * Gc.stride[d];
+    }
+    if (w == 0.f) continue;
+    const float* row = cb + off;
+    if (nfy == ncy) {
+      const float4 t = *reinterpret_cast<const float4*>(row + y0);
+      acc[0] += w * t.x; acc[1] += w * t.y; acc[2] += w * t.z; acc[3] += w * t.w;
+    } else if ((nfy & 1) == 0) {  // cell-centred: window 2q-1 .. 2q+2, clamped
+      const float c0 = __ldg(row + max(q2 - 1, 0)), c1 = __ldg(row + q2);
+      const float c2 = __ldg(row + min(q2 + 1, ncy - 1)), c3 = __ldg(row + min(q2 + 2, ncy - 1));
+      acc[0] += w * (0.75f * c1 + 0.25f * c0);
+      acc[1] += w * (0.75f * c1 + 0.25f * c2);
+      acc[2] += w * (0.75f * c2 + 0.25f * c1);
+      acc[3] += w * (0.75f * c2 + 0.25f * c3);
+    } else {  // vertex-centred: window 2q .. 2q+2
+      const float c0 = __ldg(row + q2), c1 = __ldg(row + min(q2 + 1, ncy - 1));
+      const float c2 = __ldg(row + min(q2 + 2, ncy - 1));
+      acc[0] += w * c0;
+      acc[1] += w * 0.5f * (c0 + c1);
+      acc[2] += w * c1;
+      acc[3] += w * 0.5f * (c1 + c2);
+    }
+  }
+  *reinterpret_cast<float4*>(fine + (size_t)v * Pf + p0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+}
+
+// quad kernels need the last axis % 4 == 0 on the output side (and on the fine side for the
+// restriction's float4 window)
+static inline bool transfer_quads(const Geo& Gf, const Geo& Gc) {
+  const int L = Gf.D - 1;
+  return (Gf.n[L] % 4 == 0) && (Gc.n[L] % 4 == 0);
+}
+
 void launch_restrict1(const Geo& Gf, const Geo& Gc, int nvec, const float* fine, float* coarse,
                       const int* act, cudaStream_t s) {
   ++g_launch_count;
+  if (transfer_quads(Gf, Gc)) {
+    const dim3 gq((Gc.P / 4 + 255) / 256, nvec);
+    if (Gf.D == 2)
+      k_restrict1q<2><<<gq, 256, 0, s>>>(Gf, Gc, fine, coarse, act);
+    else
+      k_restrict1q<3><<<gq, 256, 0, s>>>(Gf, Gc, fine, coarse, act);
+    return;
+  }
   const dim3 g((Gc.P + 255) / 256, nvec);
   if (Gf.D == 2)
     k_restrict1<2><<<g, 256, 0, s>>>(Gf, Gc, fine, coarse, act);
@@ -321,6 +453,14 @@ void launch_restrict1(const Geo& Gf, const Geo& Gc, int nvec, const float* fine,
 void launch_prolong1(const Geo& Gf, const Geo& Gc, int nvec, const float* coarse, float* fine,
                      const int* act, cudaStream_t s) {
   ++g_launch_count;
+  if (transfer_quads(Gf, Gc)) {
+    const dim3 gq((Gf.P / 4 + 255) / 256, nvec);
+    if (Gf.D == 2)
+      k_prolong1q<2><<<gq, 256, 0, s>>>(Gf, Gc, coarse, fine, act);
+    else
+      k_prolong1q<3><<<gq, 256, 0, s>>>(Gf, Gc, coarse, fine, act);
+    return;
+  }
   const dim3 g((Gf.P + 255) / 256, nvec);
   if (Gf.D == 2)
     k_prolong1<2><<<g, 256, 0, s>>>(Gf, Gc, coarse, fine, act);

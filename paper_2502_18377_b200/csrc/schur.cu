@@ -315,7 +315,7 @@ __device__ __forceinline__ int block_points(int remap, int P, int nlast, int p0_
     const int R = kThreads / (nlast >> 2), rows = P / nlast;
     return max(0, min(R, rows - (int)blockIdx.x * R)) * nlast;
   }
-  return min(4 * kThreads, P - p0_first);
+  return min(4 * (int)blockDim.x, P - p0_first);
 }
 
 template <int D, typename T>
@@ -945,7 +945,7 @@ __device__ __forceinline__ double quad_epilogue(const EpiArgs& A, int pde, size_
   return dot;
 }
 
-template <int EPI, int BX, int NX, int NY>
+template <int EPI, int BX, int NX, int NY, int YP>
 __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __restrict__ cf, int crep,
                                                          const float* __restrict__ x,
                                                          const float* __restrict__ hb, EpiArgs A,
@@ -999,7 +999,15 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __
       for (int b = 0; b < BX + 1; ++b) {
         if ((a && !okt) || (b && !okx)) continue;
         const int p0 = pb + a * st + b * sxs;
-        quad_y_own<NX, NY>(G, cb, xb, hv, p0, t0 + a, x0 + b, acc[a][b], ymode);
+        if (YP) {  // y-axis and own terms from pass 1 (k_schur_hy)
+          const float4 r = ld4(hv + (size_t)gridDim.y * P + p0);
+          acc[a][b][0] += r.x;
+          acc[a][b][1] += r.y;
+          acc[a][b][2] += r.z;
+          acc[a][b][3] += r.w;
+        } else {
+          quad_y_own<NX, NY>(G, cb, xb, hv, p0, t0 + a, x0 + b, acc[a][b], ymode);
+        }
         dot += quad_epilogue<EPI>(A, pde, (size_t)v * P + p0, x, acc[a][b]);
         ++nq;
       }
@@ -1605,6 +1613,107 @@ __global__ void __launch_bounds__(4 * NY) k_schur_s_tile(Geo G, const float* __r
   }
 }
 
+// ---------------------------------------------------------------------------------
+// 3D fp32 pass 1 with the y-axis (contiguous) part of S folded in ("hy"): a CTA covers
+// R = kThreads / (n_y/4) whole rows (remap_quad mapping).  Each thread computes h of its
+// quad, parks x, u~_y1 h, u~_y2 h of the quad in shared memory, and after one barrier
+// evaluates  r_y = P0_y x - K_y^T (u~_y h) + sigma alpha h + w_bnd^2 [B] x  from the smem rows
+// (no neighbour h from HBM).  Writes h and r_y (second half of the 8-byte-per-point g
+// buffer); pass 2 then needs only the t and x axes (fewer registers, no y windows).
+// ---------------------------------------------------------------------------------
+template <int NX, int NY>
+__global__ void __launch_bounds__(kThreads) k_schur_hy(Geo G, const float* __restrict__ cf, int crep,
+                                                      const float* __restrict__ x,
+                                                      float* __restrict__ gout, const int* act,
+                                                      unsigned long long* pts) {
+  __shared__ __align__(16) float sx[4 * kThreads], sw1[4 * kThreads], sw2[4 * kThreads],
+      sh[4 * kThreads];
+  const int v = blockIdx.y, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  const int nl = dim_n<NX, NY>(G, 2), NY4 = nl >> 2;
+  if (pts && threadIdx.x == 0) atomicAdd(pts, (unsigned long long)block_points(1, P, nl, 0));
+  const float* cb = cf + (size_t)pde * 8 * P;
+  const float* xb = x + (size_t)v * P;
+  {  // phase 1, natural mapping (coalesced): h of this thread's quad -> HBM and smem
+    const int pn = (blockIdx.x * kThreads + threadIdx.x) * 4;
+    if (pn < P) {
+      int id[3];
+      unravel<3>(G, pn, id);
+      float hn[4];
+      schur_h4<3, float>(G, cb, xb, pn, id, hn, 0);
+      st4(gout + (size_t)v * P + pn, hn);
+      const float4 u1 = ld4(cb + 6 * (size_t)P + pn), u2 = ld4(cb + 7 * (size_t)P + pn);
+      const int so = 4 * threadIdx.x;  // CTA rows are contiguous: smem index = pn - CTA base
+      sts4(sx + so, ld4(xb + pn));
+      sts4(sh + so, make_float4(hn[0], hn[1], hn[2], hn[3]));
+      sts4(sw1 + so, make_float4(u1.x * hn[0], u1.y * hn[1], u1.z * hn[2], u1.w * hn[3]));
+      sts4(sw2 + so, make_float4(u2.x * hn[0], u2.y * hn[1], u2.z * hn[2], u2.w * hn[3]));
+    }
+  }
+  __syncthreads();
+  // phase 2, warp-specialised mapping (interior / edge y quads), operands from smem
+  int row, q, ymode;
+  remap_quad(NY4, row, q, ymode);
+  const int lr = row - (int)blockIdx.x * (kThreads / NY4), y0 = 4 * q;
+  const int p0 = row * nl + y0;
+  if (p0 >= P) return;
+  int idx[3];
+  unravel<3>(G, p0, idx);
+  const float* sxr = sx + lr * nl;
+  const float* sw1r = sw1 + lr * nl;
+  const float* sw2r = sw2 + lr * nl;
+  const float4 hv4 = lds4(sh + lr * nl + y0), csa = ld4(cb + p0);
+  const float hq[4] = {hv4.x, hv4.y, hv4.z, hv4.w};
+  float xw[20], aw[12], bw[12];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int off = y0 - 8 + 4 * k;
+    const bool ok = ymode == 1 || (off >= 0 && off < nl);
+    const float4 vv = ok ? lds4(sxr + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    xw[4 * k] = vv.x; xw[4 * k + 1] = vv.y; xw[4 * k + 2] = vv.z; xw[4 * k + 3] = vv.w;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int off = y0 - 4 + 4 * k;
+    const bool ok = ymode == 1 || (off >= 0 && off < nl);
+    const float4 va = ok ? lds4(sw1r + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 vb = ok ? lds4(sw2r + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    aw[4 * k] = va.x; aw[4 * k + 1] = va.y; aw[4 * k + 2] = va.z; aw[4 * k + 3] = va.w;
+    bw[4 * k] = vb.x; bw[4 * k + 1] = vb.y; bw[4 * k + 2] = vb.z; bw[4 * k + 3] = vb.w;
+  }
+  float ry[4];
+  const bool face = (idx[0] == 0) | (idx[0] == G.n[0] - 1) | (idx[1] == 0) |
+                    (idx[1] == dim_n<NX, NY>(G, 1) - 1);
+  const float wb2 = G.wb * G.wb;
+  const float sav[4] = {csa.x, csa.y, csa.z, csa.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float a = sav[j] * hq[j];
+    if (face || y0 + j == 0 || y0 + j == nl - 1) a += wb2 * xw[8 + j];
+    if (ymode == 1) {
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) a += G.irow[2][20 + o + 4] * xw[8 + j + o];
+#pragma unroll
+      for (int o = -2; o <= 2; ++o)
+        a -= G.irow[2][10 + (o + 2) * 2] * aw[4 + j + o] + G.irow[2][10 + (o + 2) * 2 + 1] * bw[4 + j + o];
+    } else {
+      const float* rowp = tab_row(G, 2, y0 + j);
+      float p0r[12], ktr[20];
+      ldv<3>(rowp + kTabP0, p0r);
+      ldv<5>(rowp + kTabKT, ktr);
+#pragma unroll
+      for (int o = -5; o <= 5; ++o) a += p0r[o + 5] * xw[8 + j + o];
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        if (4 + j + o < 0 || 4 + j + o > 11) continue;
+        a -= ktr[(o + 4) * 2] * aw[4 + j + o] + ktr[(o + 4) * 2 + 1] * bw[4 + j + o];
+      }
+    }
+    ry[j] = a;
+  }
+  st4(gout + (size_t)gridDim.y * P + (size_t)v * P + p0, ry);
+}
+
 // ------------------------------------------------------------------------- launchers
 static inline dim3 grid2(int P, int nvec) { return dim3((P + kThreads - 1) / kThreads, nvec); }
 
@@ -1625,10 +1734,15 @@ void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStrea
 }
 
 static inline bool use_v4(const Geo& G) { return (G.n[G.D - 1] & 3) == 0; }
+// small levels (<= 16384 points per vector): 4-points-per-thread kernels in 64-thread CTAs
+// (a 256-thread CTA per PDE leaves most SMs idle at the coarse levels)
+constexpr int kSmallP = 16384, kSmallThreads = 64;
+static inline bool small_level(const Geo& G) { return G.P <= kSmallP; }
+static inline int v4_threads(const Geo& G) { return small_level(G) ? kSmallThreads : kThreads; }
 // warp-specialised interior / edge quads (remap_quad): NY4 a power of two dividing kThreads
 static inline int use_remap(const Geo& G) {
   const int q = G.n[G.D - 1] >> 2;
-  return use_v4(G) && q > 0 && (q & (q - 1)) == 0 && q <= kThreads;
+  return use_v4(G) && !small_level(G) && q > 0 && (q & (q - 1)) == 0 && q <= kThreads;
 }
 // 2x2 (t,x)-blocked pass 2: 3D, fp32, n_y % 4 == 0
 static int g_block_mode = -1;  // 0: v4, 1: 2x1 (t), 2: 2x2 (t,x); env MPDE_SCHUR_BLOCK
@@ -1640,7 +1754,7 @@ static inline int block_mode() {
   return g_block_mode;
 }
 static inline bool use_b22(const Geo& G, bool f64) {
-  return G.D == 3 && !f64 && use_v4(G) && block_mode() > 0;
+  return G.D == 3 && !f64 && use_v4(G) && !small_level(G) && block_mode() > 0;
 }
 static inline int b22_threads(const Geo& G) {
   const int bx = block_mode() == 2;
@@ -1664,6 +1778,16 @@ static inline int b22_ctas(const Geo& G) {
   const int R = kThreads / (G.n[2] / 4), XPB = R / tp;
   return ((G.n[0] + 1) / 2 + tp - 1) / tp * ((G.n[1] + XPB - 1) / XPB);
 }
+// pass 1 with the y part folded in (k_schur_hy) + pass 2 on t and x only: the t-blocked
+// pass-2 levels with the warp-specialised mapping (env MPDE_HY=0 disables)
+static int g_hy = -1;
+static inline bool use_hy(const Geo& G, bool f64) {
+  if (g_hy < 0) {
+    const char* e = getenv("MPDE_HY");
+    g_hy = e ? atoi(e) : 0;
+  }
+  return g_hy && use_b22(G, f64) && block_mode() == 1 && use_remap(G);
+}
 // fused single-kernel S apply (k_schur_fused): 3D fp32 levels with full-row tiles
 static int g_fused = -1;  // env MPDE_FUSED=1 enables (default off: slower)
 static inline bool use_fused(const Geo& G, bool f64) {
@@ -1672,7 +1796,7 @@ static inline bool use_fused(const Geo& G, bool f64) {
     g_fused = e ? atoi(e) : 0;
   }
   const int n1 = G.D == 3 ? G.n[1] : 0, n2 = G.D == 3 ? G.n[2] : 0;
-  return g_fused && G.D == 3 && !f64 && n2 % 4 == 0 && n2 >= 32 && n2 <= 128 &&
+  return g_fused && G.D == 3 && !f64 && !small_level(G) && n2 % 4 == 0 && n2 >= 32 && n2 <= 128 &&
          n1 % kFX == 0 && n1 >= 2 * kFX;
 }
 bool schur_fused(const Geo& G, bool f64) { return use_fused(G, f64); }
@@ -1683,7 +1807,7 @@ static inline bool use_tile(const Geo& G, bool f64) {
     const char* e = getenv("MPDE_TILE");
     g_tile = e ? atoi(e) : 0;
   }
-  if (!g_tile || G.D != 3 || f64) return false;
+  if (!g_tile || G.D != 3 || f64 || small_level(G)) return false;
   const int n2 = G.n[2];
   return (n2 == 32 || n2 == 64 || n2 == 128) && G.n[1] % kTX == 0 && G.n[1] >= 2 * kTX;
 }
@@ -1692,18 +1816,35 @@ int schur_tiles(const Geo& G, bool f64) {
   if (use_fused(G, f64)) return G.n[1] / kFX;
   if (use_tile(G, f64)) return tile_ctas(G);
   if (use_b22(G, f64)) return b22_ctas(G);
-  return use_v4(G) ? (G.P + 4 * kThreads - 1) / (4 * kThreads) : (G.P + kThreads - 1) / kThreads;
+  if (use_v4(G)) {
+    const int th = v4_threads(G);
+    return (G.P + 4 * th - 1) / (4 * th);
+  }
+  return (G.P + kThreads - 1) / kThreads;
 }
 
 void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const float* x, void* g,
                     const int* act, unsigned long long* pts, bool f64, cudaStream_t s) {
   ++g_launch_count;
-  if (use_v4(G)) {
-    dim3 gr((G.P + 4 * kThreads - 1) / (4 * kThreads), nvec);
-    if (f64)
-      DISPATCH_D2(G.D, k_schur_h_v4<DD, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (double*)g, act, pts, 0));
+  if (use_hy(G, f64)) {
+    const dim3 gr((G.P + 4 * kThreads - 1) / (4 * kThreads), nvec);
+    if (G.n[1] == 64 && G.n[2] == 64)
+      k_schur_hy<64, 64><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (float*)g, act, pts);
+    else if (G.n[1] == 32 && G.n[2] == 32)
+      k_schur_hy<32, 32><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (float*)g, act, pts);
+    else if (G.n[1] == 128 && G.n[2] == 128)
+      k_schur_hy<128, 128><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (float*)g, act, pts);
     else
-      DISPATCH_D2(G.D, k_schur_h_v4<DD, float><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (float*)g, act, pts, 0));
+      k_schur_hy<0, 0><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (float*)g, act, pts);
+    return;
+  }
+  if (use_v4(G)) {
+    const int th = v4_threads(G);
+    dim3 gr((G.P + 4 * th - 1) / (4 * th), nvec);
+    if (f64)
+      DISPATCH_D2(G.D, k_schur_h_v4<DD, double><<<gr, th, 0, s>>>(G, cf, crep, x, (double*)g, act, pts, 0));
+    else
+      DISPATCH_D2(G.D, k_schur_h_v4<DD, float><<<gr, th, 0, s>>>(G, cf, crep, x, (float*)g, act, pts, 0));
     return;
   }
   if (f64)
@@ -1750,21 +1891,23 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
   if (use_b22(G, f64)) {
     const dim3 gb(schur_tiles(G, f64), nvec);
     const int rm = use_remap(G) ? b22_tp(G) : 0;  // >1: t-pair tiling (remap implied)
-#define B22_LAUNCH(E, BXv)                                                                   \
+#define B22_LAUNCH(E, BXv, YPv)                                                              \
   if (G.n[1] == 64 && G.n[2] == 64)                                                          \
-    k_schur_s_b22<E, BXv, 64, 64><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
+    k_schur_s_b22<E, BXv, 64, 64, YPv><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
   else if (G.n[1] == 32 && G.n[2] == 32)                                                     \
-    k_schur_s_b22<E, BXv, 32, 32><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
+    k_schur_s_b22<E, BXv, 32, 32, YPv><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
   else if (G.n[1] == 128 && G.n[2] == 128)                                                   \
-    k_schur_s_b22<E, BXv, 128, 128><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
+    k_schur_s_b22<E, BXv, 128, 128, YPv><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm); \
   else                                                                                       \
-    k_schur_s_b22<E, BXv, 0, 0><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm);
+    k_schur_s_b22<E, BXv, 0, 0, YPv><<<gb, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm);
 #define B22_CASE(E)                                                                          \
   case E:                                                                                    \
     if (block_mode() == 2) {                                                                 \
-      B22_LAUNCH(E, 1)                                                                       \
+      B22_LAUNCH(E, 1, 0)                                                                    \
+    } else if (use_hy(G, f64)) {                                                             \
+      B22_LAUNCH(E, 0, 1)                                                                    \
     } else {                                                                                 \
-      B22_LAUNCH(E, 0)                                                                       \
+      B22_LAUNCH(E, 0, 0)                                                                    \
     }                                                                                        \
     break;
     switch (epi) {
@@ -1782,14 +1925,15 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
   }
   const bool v4 = use_v4(G);
   const int rm = use_remap(G);
+  const int th = v4 ? v4_threads(G) : kThreads;
   dim3 gr(schur_tiles(G, f64), nvec);
 #define EPI_CASE2(E)                                                                              \
   case E:                                                                                         \
     if (v4) {                                                                                     \
       if (f64)                                                                                    \
-        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const double*)g, A, act, rm)); \
+        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, double><<<gr, th, 0, s>>>(G, cf, crep, x, (const double*)g, A, act, rm)); \
       else                                                                                        \
-        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, float><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm)); \
+        DISPATCH_D2(G.D, k_schur_s_v4<DD, E, float><<<gr, th, 0, s>>>(G, cf, crep, x, (const float*)g, A, act, rm)); \
     } else if (f64)                                                                               \
       DISPATCH_D2(G.D, k_schur_s<DD, E, double><<<gr, kThreads, 0, s>>>(G, cf, crep, x, (const double*)g, A, act)); \
     else                                                                                          \
