@@ -946,7 +946,7 @@ __device__ __forceinline__ double quad_epilogue(const EpiArgs& A, int pde, size_
 }
 
 template <int EPI, int BX, int NX, int NY, int YP>
-__global__ void __launch_bounds__(kThreads) k_schur_s_b22(Geo G, const float* __restrict__ cf, int crep,
+__global__ void __launch_bounds__(kThreads, 3) k_schur_s_b22(Geo G, const float* __restrict__ cf, int crep,
                                                          const float* __restrict__ x,
                                                          const float* __restrict__ hb, EpiArgs A,
                                                          const int* act, int remap) {
@@ -1809,6 +1809,7 @@ static inline bool use_tile(const Geo& G, bool f64) {
   }
   if (!g_tile || G.D != 3 || f64 || small_level(G)) return false;
   const int n2 = G.n[2];
+  if (g_tile == 2 && n2 > 32) return false;  // 2: only the n_y = 32 levels
   return (n2 == 32 || n2 == 64 || n2 == 128) && G.n[1] % kTX == 0 && G.n[1] >= 2 * kTX;
 }
 static inline int tile_ctas(const Geo& G) { return ((G.n[0] + kTT - 1) / kTT) * (G.n[1] / kTX); }
