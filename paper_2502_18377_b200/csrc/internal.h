@@ -123,6 +123,7 @@ void launch_p_update(int P, int nvec, const float* beta, const float* z, float* 
                      const int* act, cudaStream_t s);
 void launch_scale(int P, int nvec, const float* sc, const float* x, float* y, const int* act,
                   cudaStream_t s);
+void launch_add(int P, int nvec, const float* x, float* y, const int* act, cudaStream_t s);
 void launch_lz_update(int P, int nvec, const float* y, const float* v, float* vprev,
                       const float* dinv, const float* alpha, const float* beta, double* part,
                       cudaStream_t s);

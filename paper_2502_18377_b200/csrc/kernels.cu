@@ -503,6 +503,17 @@ __global__ void __launch_bounds__(kThreads) k_p_update(int P, const float* __res
   p_[o] = b == 0.f ? z[o] : z[o] + b * p_[o];  // p_old may be uninitialised when b == 0
 }
 
+// y += x (W-cycle: sum of the two coarse corrections)
+__global__ void __launch_bounds__(kThreads) k_add(int P, const float* __restrict__ x, float* y,
+                                                 const int* act) {
+  const int v = blockIdx.y;
+  if (act && !act[v]) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const size_t o = (size_t)v * P + p;
+  y[o] += x[o];
+}
+
 // generic: y = a*x (per-vector scale), or fill
 __global__ void __launch_bounds__(kThreads) k_scale(int P, const float* __restrict__ s,
                                                    const float* __restrict__ x, float* y,
@@ -989,6 +1000,10 @@ void launch_p_update(int P, int nvec, const float* beta, const float* z, float* 
                      const int* act, cudaStream_t s) {
   ++g_launch_count;
   k_p_update<<<grid_for(P, nvec), kThreads, 0, s>>>(P, beta, z, p, act);
+}
+void launch_add(int P, int nvec, const float* x, float* y, const int* act, cudaStream_t s) {
+  ++g_launch_count;
+  k_add<<<grid_for(P, nvec), kThreads, 0, s>>>(P, x, y, act);
 }
 void launch_scale(int P, int nvec, const float* sc, const float* x, float* y, const int* act,
                   cudaStream_t s) {

@@ -304,6 +304,8 @@ struct Level {
   double* lmax;     // [B]
   float* coef;      // [B][2 nu]
   float *r, *e, *d, *d2, *g, *pe;  // [B][P]
+  float* rr = nullptr;  // W-cycle: restricted residual kept (levels >= 1)
+  float* ew = nullptr;  // W-cycle: first coarse correction
   float* cf;        // [B][2+2D][P] per-point coefficients of S (schur.cu)
   float* tab;       // device row tables of S, sum_d n_d * kTabRow floats
   std::vector<float> tab_host;
@@ -379,6 +381,10 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
     lv.d2 = bp.take<float>((size_t)B * lv.P);
     lv.g = bp.take<float>((size_t)2 * B * lv.P);  // 8 bytes per point (fp64 g)
     lv.pe = bp.take<float>((size_t)B * lv.P);
+    if (l > 0) {  // W-cycle visits of this level: restricted rhs kept, first correction saved
+      lv.rr = bp.take<float>((size_t)B * lv.P);
+      lv.ew = bp.take<float>((size_t)B * lv.P);
+    }
   }
   h->sinv = bp.take<float>((size_t)B * Pc * Pc);
   h->x = bp.take<float>((size_t)B * P);
@@ -462,6 +468,16 @@ int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const flo
 
 // One V-cycle on level l for rhs `rin` (level 0: PCG residual, copied), writing the
 // correction into lv.e.  rdot/part: optional <rdot, e> partials from the last kernel.
+// levels l < wcycle_levels() use gamma = 2 (env MPDE_WCYCLE, default 0 = V-cycle)
+static int wcycle_levels() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("MPDE_WCYCLE");
+    w = e ? atoi(e) : 0;
+  }
+  return w;
+}
+
 int vcycle(mpde_hierarchy* h, int l, const float* rin, const float* rdot, double* part,
            const int* act, cudaStream_t s) {
   const int B = h->B;
@@ -491,9 +507,24 @@ int vcycle(mpde_hierarchy* h, int l, const float* rin, const float* rdot, double
   }
   // residual after pre-smoothing, restrict
   if (int rc = schur_apply(h, l, EPI_RESID, B, 1, dcur, A, act, f64_vcycle(h), s)) return rc;
-  PROF(5, s, launch_restrict1(lv.G, lc.G, B, lv.r, lc.r, act, s));
-  CKL();
-  if (int rc = vcycle(h, l + 1, lc.r, nullptr, nullptr, act, s)) return rc;
+  if (l < wcycle_levels() && l + 1 < h->L - 1) {
+    // gamma = 2 at this level (W-cycle): e_c = B r_c + B (r_c - S_c B r_c), B = the coarse
+    // cycle; symmetric (2B - B S_c B), so the preconditioner stays a fixed SPD map
+    PROF(5, s, launch_restrict1(lv.G, lc.G, B, lv.r, lc.rr, act, s));
+    CKL();
+    if (int rc = vcycle(h, l + 1, lc.rr, nullptr, nullptr, act, s)) return rc;
+    CK(cudaMemcpyAsync(lc.ew, lc.e, sizeof(float) * (size_t)B * lc.P, cudaMemcpyDeviceToDevice, s));
+    EpiArgs Ac;
+    Ac.res = lc.rr;
+    if (int rc = schur_apply(h, l + 1, EPI_RESID, B, 1, lc.ew, Ac, act, f64_vcycle(h), s)) return rc;
+    if (int rc = vcycle(h, l + 1, lc.rr, nullptr, nullptr, act, s)) return rc;
+    PROF(6, s, launch_add(lc.P, B, lc.ew, lc.e, act, s));
+    CKL();
+  } else {
+    PROF(5, s, launch_restrict1(lv.G, lc.G, B, lv.r, lc.r, act, s));
+    CKL();
+    if (int rc = vcycle(h, l + 1, lc.r, nullptr, nullptr, act, s)) return rc;
+  }
   PROF(5, s, launch_prolong1(lv.G, lc.G, B, lc.e, lv.pe, act, s));
   CKL();
   // post-smoothing: e += P e_c; res -= S (P e_c); d0 = beta0 Dinv res; e += d0

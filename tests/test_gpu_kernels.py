@@ -68,15 +68,20 @@ np.save(sys.argv[2], y.cpu().numpy())
 """
 
 
-@pytest.mark.parametrize("shape,h,fused", [
-    ((7, 16, 32), (0.05, 0.06, 0.07), "1"),   # fused, 2 x-tiles
-    ((9, 24, 36), (0.04, 0.03, 0.05), "1"),   # fused, interior tile
-    ((7, 16, 64), (0.05, 0.06, 0.07), "0"),   # t-blocked pass 2, warp-specialised y quads (NY4=16)
-    ((8, 10, 32), (0.05, 0.06, 0.07), "0")])  # t-blocked pass 2, NY4=8 (4 interior / 4 edge)
-def test_large_schur_matches_sparse(shape, h, fused, tmp_path):
-    """S apply at n_y >= 32 (the warp-specialised and the fused single-kernel paths; the kernel
-    selection MPDE_FUSED is read once per process, so the apply runs in a child process)
-    against S applied through the oracle's sparse A (no dense N at these sizes)."""
+@pytest.mark.parametrize("shape,h,env", [
+    ((7, 16, 32), (0.05, 0.06, 0.07), {"MPDE_FUSED": "1"}),   # fused, 2 x-tiles
+    ((9, 24, 36), (0.04, 0.03, 0.05), {"MPDE_FUSED": "1"}),   # fused, interior tile
+    ((7, 16, 64), (0.05, 0.06, 0.07), {}),                    # t-blocked pass 2, warp-specialised y (NY4=16)
+    ((8, 10, 32), (0.05, 0.06, 0.07), {}),                    # t-blocked pass 2, NY4=8 (4 interior / 4 edge)
+    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_HY": "1"}),      # y part in pass 1
+    ((9, 12, 32), (0.05, 0.06, 0.07), {"MPDE_HY": "1"}),
+    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_TILE": "1"}),    # smem-tiled pass 2
+    ((13, 12, 32), (0.05, 0.06, 0.07), {"MPDE_TILE": "1"}),   # partial last t tile
+    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_B22_TP": "4"})])  # t-pair CTA tiling
+def test_large_schur_matches_sparse(shape, h, env, tmp_path):
+    """S apply at n_y >= 32 through every 3D kernel variant (the selection switches are read
+    once per process, so the apply runs in a child process) against S applied through the
+    oracle's sparse A (no dense N at these sizes)."""
     import os
     import subprocess
     import sys
@@ -88,7 +93,7 @@ def test_large_schur_matches_sparse(shape, h, fused, tmp_path):
     w = (1.25, 2.0, 0.75, 0.875)
     x = rng.normal(size=(B, P)).astype(np.float32)
     np.savez(tmp_path / "in.npz", shape=np.array(shape), h=np.array(h), w=np.array(w), c=c, x=x)
-    env = dict(os.environ, MPDE_FUSED=fused)
+    env = dict(os.environ, **env)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.run([sys.executable, "-c", _APPLY_SCRIPT, str(tmp_path / "in.npz"),
                     str(tmp_path / "y.npy")], check=True, env=env, cwd=root)
@@ -121,3 +126,35 @@ def test_vcycle_symmetric_positive(shape, h):
         assert abs(l - r) <= 1e-4 * (abs(l) + abs(r))
         assert float((ma[i].double() * a[i].double()).sum()) > 0
     s.close()
+
+
+_PRECOND_SCRIPT = r"""
+import sys, numpy as np, torch
+from paper_2502_18377_b200 import mpde
+rng = np.random.default_rng(6)
+shape, B = (16, 18, 20), 2
+P = int(np.prod(shape))
+c = rng.normal(0.0, 0.5, (B, 7, P)); c[:, 1] += 1.0
+s = mpde.Solver(shape, (0.05, 0.06, 0.07), torch.from_numpy(c.astype(np.float32)).cuda())
+a = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()
+b = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()
+ma, mb = torch.empty_like(a), torch.empty_like(b)
+mpde.mpde_apply_precond(s.h_, a, ma); mpde.mpde_apply_precond(s.h_, b, mb)
+torch.cuda.synchronize()
+for i in range(B):
+    l = float((ma[i].double() * b[i].double()).sum()); r = float((a[i].double() * mb[i].double()).sum())
+    assert abs(l - r) <= 1e-4 * (abs(l) + abs(r)), (l, r)
+    assert float((ma[i].double() * a[i].double()).sum()) > 0
+print("ok")
+"""
+
+
+def test_wcycle_symmetric_positive():
+    """The W-cycle option (MPDE_WCYCLE=1: gamma = 2 below level 0) is still a fixed SPD map."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _PRECOND_SCRIPT], check=True, cwd=root,
+                         env=dict(os.environ, MPDE_WCYCLE="1"), capture_output=True, text=True)
+    assert "ok" in out.stdout
