@@ -202,12 +202,14 @@ int mpde_batch_sum(const float* x, int32_t batch, int64_t n, float* out, mpde_st
 /* ---- launch profiler (process-wide, not thread-safe; off by default) ------------
  * Between begin and end every library launch is bracketed by CUDA events on the
  * stream it is launched on.  end() synchronises and returns, per launch class,
- * the summed event time (ms) and the launch count; pts[0..7] = points processed by the
- * S pass-2 kernel per epilogue kind, pts[8] = points processed by the S pass-1 kernel.
- * Classes: 0 S pass 1 (schur_g), 1 S pass 2 (schur_out), 2 fp64 residual, 3 condense,
- * 4 back-substitution, 5 grid transfers, 6 PCG/smoother vector ops, 7 per-PDE scalar
- * logic, 8 coarsest solve, 9 hierarchy build, 10 forward/backward epilogues. */
-#define MPDE_PROF_NCLASS 11
+ * the summed event time (ms) and the launch count; pts[0..6] = points processed by the
+ * S pass-2 kernel per epilogue kind on levels >= 1, pts[9..15] the same on level 0,
+ * pts[8] / pts[7] = points processed by the S pass-1 kernel on levels >= 1 / level 0.
+ * Classes: 0 S pass 1 (schur_g, levels >= 1), 1 S pass 2 (schur_out, levels >= 1),
+ * 2 fp64 residual, 3 condense, 4 back-substitution, 5 grid transfers, 6 PCG/smoother
+ * vector ops, 7 per-PDE scalar logic, 8 coarsest solve, 9 hierarchy build,
+ * 10 forward/backward epilogues, 11 S pass 2 on level 0, 12 S pass 1 on level 0. */
+#define MPDE_PROF_NCLASS 13
 /* Number of kernel launches this process has issued through the library so far. */
 uint64_t mpde_launch_count(void);
 int mpde_profile_begin(void);

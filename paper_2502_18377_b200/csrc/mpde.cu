@@ -453,15 +453,17 @@ int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const flo
                 const EpiArgs& A, const int* act, bool f64, cudaStream_t s) {
   Level& lv = h->lv[l];
   EpiArgs A2 = A;
-  A2.pts = g_prof.on ? g_prof.d_pts : nullptr;
+  // profiling: level 0 has its own classes (11 pass 2, 12 pass 1) and point counters
+  A2.pts = g_prof.on ? g_prof.d_pts + (l == 0 ? 9 : 0) : nullptr;
+  const int c_out = l == 0 ? 11 : 1, c_g = l == 0 ? 12 : 0;
   if (schur_fused(lv.G, f64)) {
-    PROF(1, s, launch_schur_fused(epi, lv.G, nvec, crep, lv.cf, x, A2, act, s));
+    PROF(c_out, s, launch_schur_fused(epi, lv.G, nvec, crep, lv.cf, x, A2, act, s));
     CKL();
     return MPDE_OK;
   }
-  PROF(0, s, launch_schur_g(lv.G, nvec, crep, lv.cf, x, lv.g, act, A2.pts ? A2.pts + 8 : nullptr,
-                            f64, s));
-  PROF(1, s, launch_schur_out(epi, lv.G, nvec, crep, lv.cf, x, lv.g, A2, act, f64, s));
+  PROF(c_g, s, launch_schur_g(lv.G, nvec, crep, lv.cf, x, lv.g, act,
+                              g_prof.on ? g_prof.d_pts + (l == 0 ? 7 : 8) : nullptr, f64, s));
+  PROF(c_out, s, launch_schur_out(epi, lv.G, nvec, crep, lv.cf, x, lv.g, A2, act, f64, s));
   CKL();
   return MPDE_OK;
 }

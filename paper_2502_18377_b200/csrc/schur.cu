@@ -1736,8 +1736,15 @@ void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStrea
 static inline bool use_v4(const Geo& G) { return (G.n[G.D - 1] & 3) == 0; }
 // small levels (<= 16384 points per vector): 4-points-per-thread kernels in 64-thread CTAs
 // (a 256-thread CTA per PDE leaves most SMs idle at the coarse levels)
-constexpr int kSmallP = 16384, kSmallThreads = 64;
-static inline bool small_level(const Geo& G) { return G.P <= kSmallP; }
+constexpr int kSmallThreads = 64;
+static int g_small_p = -1;  // points-per-vector threshold (env MPDE_SMALLP, default 16384)
+static inline bool small_level(const Geo& G) {
+  if (g_small_p < 0) {
+    const char* e = getenv("MPDE_SMALLP");
+    g_small_p = e ? atoi(e) : 16384;
+  }
+  return G.P <= g_small_p;
+}
 static inline int v4_threads(const Geo& G) { return small_level(G) ? kSmallThreads : kThreads; }
 // warp-specialised interior / edge quads (remap_quad): NY4 a power of two dividing kThreads
 static inline int use_remap(const Geo& G) {

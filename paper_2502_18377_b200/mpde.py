@@ -84,7 +84,7 @@ EXPORTS = ["mpde_default_options", "mpde_sizes", "mpde_workspace_bytes", "mpde_b
            "mpde_host_staging_bytes", "mpde_fwd_bwd_host", "mpde_batch_sum",
            "mpde_profile_begin", "mpde_profile_end", "mpde_launch_count"]
 PROF_CLASSES = ["schur_g", "schur_out", "residual64", "condense", "backsub", "transfer",
-                "vector", "scalar", "coarse", "build", "epilogue"]
+                "vector", "scalar", "coarse", "build", "epilogue", "schur_out_l0", "schur_g_l0"]
 
 
 def _check(rc):
