@@ -226,6 +226,9 @@ def run_ours(a):
     fwd_its = [x[0] for x in sf]
     bwd_its = [x[0] for x in sb]
     bad = sum(1 for x in sf + sb if x[2] != 0)
+    # per-PDE stats over the job: all-reduce(max) of the slowest PDE and the failure count
+    its_max = (max_over_ranks(max(fwd_its), device=dev), max_over_ranks(max(bwd_its), device=dev))
+    bad = int(max_over_ranks(bad, device=dev))
     ms = max_over_ranks(ms, device=dev)
     ms_step = ms / a.steps
     value = world * B * a.steps / (ms / 1e3)
@@ -335,8 +338,8 @@ def run_ours(a):
                            "frac": sg_bytes / (sg_ms * 1e-3) / 1e9 / peak if sg_ms and peak else None},
             "schur_out_coarse": {"achieved_gbs": sc_bytes / (sc_ms * 1e-3) / 1e9 if sc_ms else 0.0,
                                  "launches": sc_n},
-            "iters": {"fwd_mean": sum(fwd_its) / len(fwd_its), "fwd_max": max(fwd_its),
-                      "bwd_mean": sum(bwd_its) / len(bwd_its), "bwd_max": max(bwd_its),
+            "iters": {"fwd_mean": sum(fwd_its) / len(fwd_its), "fwd_max": int(its_max[0]),
+                      "bwd_mean": sum(bwd_its) / len(bwd_its), "bwd_max": int(its_max[1]),
                       "not_converged": bad},
             "gpu_launches": launches,
             "clocks": clk,
