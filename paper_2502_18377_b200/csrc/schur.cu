@@ -1733,7 +1733,16 @@ void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStrea
   DISPATCH_D2(G.D, k_schur_coef<DD><<<grid2(G.P, B), kThreads, 0, s>>>(G, c, cf));
 }
 
-static inline bool use_v4(const Geo& G) { return (G.n[G.D - 1] & 3) == 0; }
+static inline bool small_level(const Geo& G);
+static int g_small_scalar = -1;  // env MPDE_SMALL_SCALAR=1: 1-point-per-thread kernels on small levels
+static inline bool use_v4(const Geo& G) {
+  if (g_small_scalar < 0) {
+    const char* e = getenv("MPDE_SMALL_SCALAR");
+    g_small_scalar = e ? atoi(e) : 0;
+  }
+  if (g_small_scalar && small_level(G)) return false;
+  return (G.n[G.D - 1] & 3) == 0;
+}
 // small levels (<= 16384 points per vector): 4-points-per-thread kernels in 64-thread CTAs
 // (a 256-thread CTA per PDE leaves most SMs idle at the coarse levels)
 constexpr int kSmallThreads = 64;
