@@ -208,3 +208,70 @@ def test_host_abi_matches_device_abi(gu):
     mpde.mpde_fwd_bwd_host(prob, opts, t(c), t(b), t(om), t(g), z, gc, gb, gw, stg, ws)
     assert np.array_equal(z.numpy(), dev["z"].astype(np.float32))
     assert np.array_equal(gc.numpy(), dev["grad_c"].astype(np.float32))
+
+
+# ----------------------------------------------------------------- edge cases and full size
+@pytest.mark.parametrize("shape,h,B", [((6, 6), (0.2, 0.2), 1), ((6, 6, 6), (0.2, 0.2, 0.2), 1),
+                                       ((7, 13, 10), (0.1, 0.05, 0.08), 3)])
+def test_minimal_and_odd_grids(shape, h, B, gu):
+    """Smallest admissible grid (6 points per dim: the 5-point one-sided stencils just fit,
+    one level) and odd, non-multiple-of-4 sizes (scalar kernel paths, odd coarsening)."""
+    c, b, om, g = _rand_problem(shape, B, 71)
+    out = gu.gpu_solve(shape, h, c, b, om, g)
+    pr, ref = _oracle(shape, h, c, b, om, g,
+                      method="dense" if np.prod(shape) * (1 + 2 * len(shape)) <= 5000 else "lu")
+    for i in range(B):
+        f, bw = ref[i]
+        assert gu.rel(out["z"][i], f["z"]) <= E_Z
+        for k in ("grad_c", "grad_b", "grad_omega"):
+            assert gu.rel(out[k][i], bw[k]) <= E_G, k
+
+
+def test_zero_rhs_gives_zero_solution(gu):
+    """Degenerate data: b = 0 and omega = 0 make d = 0, so z* = 0 exactly (no 0/0 in the
+    relative stopping tests); the adjoint solve still runs (g != 0) and grad_c = 0 because
+    rho = b - c.z* = 0 and z* = 0, while grad_b = w_eq^2 c.d_z matches the oracle."""
+    shape, h, B = (10, 12, 16), (0.1, 0.08, 0.07), 2
+    c, b, om, g = _rand_problem(shape, B, 81)
+    b[:] = 0.0
+    om[:] = 0.0
+    out = gu.gpu_solve(shape, h, c, b, om, g)
+    pr, ref = _oracle(shape, h, c, b, om, g, method="lu")
+    for i in range(B):
+        assert np.all(out["z"][i] == 0.0)
+        assert out["stats_fwd"][i]["status"] == "converged"
+        assert np.all(out["grad_c"][i] == 0.0)
+        assert gu.rel(out["grad_b"][i], ref[i][1]["grad_b"]) <= E_G
+        assert gu.rel(out["grad_omega"][i], ref[i][1]["grad_omega"]) <= E_G
+
+
+def test_bwd_full_size_manufactured(gu):
+    """Adjoint solve at the bench's full C4 size and batch (launch configuration of bench.py):
+    with g_z = N v for the manufactured fields v (N = A^T A applied by the oracle's CSR, fp64),
+    the exact adjoint is d_z* = v.  g_z is handed over in fp32, and N's derivative rows
+    (h^-k scaled) amplify that rounding in the derivative fields of N^-1 g (an input floor of
+    ~3e-3 there: identical with a 1e-10 solve, tools/check_bwd_floor.py), so the check is on
+    the phi field, which the paper's loss
+    reads: within 1e-4 of v.  PDEs given g_z = 0 must return d_z = 0 exactly."""
+    from oracle import normal_apply
+    m = synth.make_mms("C4")
+    cfg = m["cfg"]
+    B = m["c"].shape[0]
+    pr = Problem(cfg.shape, cfg.h)
+    M, P = 7, int(np.prod(cfg.shape))
+    g = np.zeros((B, M, P), np.float32)
+    check = (0, B - 1)
+    for i in check:
+        A, _, _ = assemble(pr, m["c"][i].astype(np.float64), m["b"][i].astype(np.float64),
+                           m["omega"][i].astype(np.float64))
+        g[i] = normal_apply(A, m["z_exact"][i].reshape(-1).astype(np.float64)).reshape(M, P) \
+            .astype(np.float32)
+    out = gu.gpu_solve(cfg.shape, cfg.h, m["c"], m["b"], m["omega"], g, want_dz=True)
+    for i in range(B):  # the PDEs with g_z = 0 must return d_z = 0 exactly
+        if i in check:
+            assert out["stats_bwd"][i]["status"] == "converged"
+            e_phi = gu.rel(out["dz"][i][0], m["z_exact"][i][0])
+            print("d_z phi error", e_phi, "all fields", gu.rel(out["dz"][i], m["z_exact"][i]))
+            assert e_phi <= E_Z
+        else:
+            assert np.all(out["dz"][i] == 0.0)
