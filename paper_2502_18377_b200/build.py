@@ -4,6 +4,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = [os.path.join(HERE, "csrc", f) for f in ("kernels.cu", "schur.cu", "dense.cu", "mpde.cu")]
@@ -12,7 +13,7 @@ DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "internal.h"
 OUT = os.path.join(HERE, "libmpde.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+         "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 
 
 def stale() -> bool:
@@ -24,10 +25,20 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC] + FLAGS + SRC + ["-o", OUT + ".tmp"]
+        # one translation unit per nvcc process (no cross-file device symbols), then link
+        objs = [os.path.join(HERE, "csrc", os.path.basename(f)[:-3] + ".o") for f in SRC]
+        cmds = [[NVCC] + FLAGS + ["-c", f, "-o", o] for f, o in zip(SRC, objs)]
         if verbose:
-            print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+            for c in cmds:
+                print(" ".join(c), file=sys.stderr)
+        with ThreadPoolExecutor(len(cmds)) as ex:
+            for r in ex.map(lambda c: subprocess.run(c), cmds):
+                if r.returncode:
+                    raise subprocess.CalledProcessError(r.returncode, r.args)
+        subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared"] + objs
+                       + ["-o", OUT + ".tmp"], check=True)
+        for o in objs:
+            os.remove(o)
         os.replace(OUT + ".tmp", OUT)
     return OUT
 

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/mpde.h"
 #include "common.cuh"
 
@@ -74,7 +76,7 @@ struct PdeState {
 };
 
 int ntiles(int P);
-extern unsigned long long g_launch_count;  // host-side count of kernel launches
+extern std::atomic<unsigned long long> g_launch_count;  // host-side count of kernel launches
 int coarse_gemv_blocks(int n);
 void upload_constants();
 

@@ -899,7 +899,7 @@ __global__ void k_stats_out(int B, PdeState st, mpde_stats* out) {
 // ----------------------------------------------------------------------------------
 static inline dim3 grid_for(int P, int nvec) { return dim3((P + kThreads - 1) / kThreads, nvec); }
 int ntiles(int P) { return (P + kThreads - 1) / kThreads; }
-unsigned long long g_launch_count = 0;
+std::atomic<unsigned long long> g_launch_count{0};
 
 void upload_constants() {
   static bool done = false;

@@ -584,16 +584,28 @@ int chunk_graph(mpde_hierarchy* h, int k, F& iteration, cudaGraphExec_t* out,
   }
   if (!g_capture_stream) CK(cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking));
   cudaGraph_t graph = nullptr;
-  const unsigned long long l0 = g_launch_count;
+  const unsigned long long l0 = g_launch_count.load();
   CK(cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeThreadLocal));
   int rc = MPDE_OK;
   for (int i = 0; i < k && rc == MPDE_OK; ++i) rc = iteration(g_capture_stream);
   const cudaError_t e = cudaStreamEndCapture(g_capture_stream, &graph);
-  const unsigned long long n = g_launch_count - l0;
-  g_launch_count = l0;  // captured, not launched: counted at every replay instead
+  // captured, not launched: the kernel nodes are counted at every replay instead
+  g_launch_count -= g_launch_count.load() - l0;
   if (rc) return rc;
   if (e != cudaSuccess)
     return set_err(MPDE_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  unsigned long long n = 0;
+  {
+    size_t cnt = 0;
+    CK(cudaGraphGetNodes(graph, nullptr, &cnt));
+    std::vector<cudaGraphNode_t> ns(cnt);
+    CK(cudaGraphGetNodes(graph, ns.data(), &cnt));
+    for (auto nd : ns) {
+      cudaGraphNodeType ty;
+      CK(cudaGraphNodeGetType(nd, &ty));
+      n += ty == cudaGraphNodeTypeKernel;
+    }
+  }
   cudaGraphExec_t exec = nullptr;
   const cudaError_t e2 = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -1005,7 +1017,7 @@ int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* d
   return set_err(MPDE_ERR_INVALID_ARG, "unknown query %d", what);
 }
 
-uint64_t mpde_launch_count(void) { return g_launch_count; }
+uint64_t mpde_launch_count(void) { return g_launch_count.load(); }
 
 int mpde_profile_begin(void) {
   if (!g_prof.d_pts) CK(cudaMalloc(&g_prof.d_pts, 16 * sizeof(unsigned long long)));
