@@ -199,6 +199,46 @@ int mpde_fwd_bwd_host(const mpde_problem* prob, const mpde_options* opts,
  * batch-summed coefficient gradient that the multi-GPU step all-reduces (NCCL). */
 int mpde_batch_sum(const float* x, int32_t batch, int64_t n, float* out, mpde_stream_t stream);
 
+/* ---- polynomial PDE-expression template ----------------------
+ * The paper builds the coefficients and the right-hand side from learned polynomials of
+ * transformed data fields u~ ("p_1(u~) = theta_0 + theta_1 u~ + theta_2 u~^2";
+ * P:520-521 third-degree polynomials of u~, v~ for the u, u_xx, u_yy coefficients and b;
+ * P:552 degree 1 for Navier-Stokes).  With F feature fields and total degree G:
+ *   c_m(p) = sum_k theta[m][k] Phi_k(u~(p))  (m < |M|),   b(p) = sum_k theta[|M|][k] Phi_k(u~(p))
+ * Phi_k = prod_f u~_f^e_f over all exponent tuples with e_0 + ... + e_{F-1} <= G, ordered by
+ * total degree, then by tuple in descending lexicographic order (F = 1: 1, u, u^2, ...;
+ * F = 2, G = 2: 1, u0, u1, u0^2, u0 u1, u1^2).  A coefficient the paper fixes (c_t = 1) is
+ * the constant monomial of its row.  theta is shared by the whole batch.
+ * Layouts (device, fp32, C-contiguous): theta [|M|+1][K]; feat [B][F][P]; coeff, grad_coeff
+ * [B][|M|][P]; rhs_b, grad_rhs [B][P]; grad_theta [|M|+1][K]; grad_feat [B][F][P].
+ * The boundary values omega are not templated (the paper takes them from u~, P:338, P:522:
+ * pass the matching feature slice as `bnd` and add grad_bnd to its gradient).
+ * Errors: MPDE_ERR_UNSUPPORTED if F not in 1..3 or G not in 0..4; MPDE_ERR_INVALID_ARG for
+ * null pointers (grad_feat may be NULL); MPDE_ERR_WORKSPACE if workspace_bytes is short. */
+typedef struct {
+  int32_t n_feat; /* F: feature fields per PDE, 1..3 */
+  int32_t degree; /* G: total polynomial degree, 0..4 */
+} mpde_template;
+
+/* K = C(F+G, G) monomials, or -1 for an unsupported template */
+int32_t mpde_template_terms(const mpde_template* t);
+
+/* coeff and rhs_b of every PDE from theta and feat (one pointwise kernel). */
+int mpde_template_coeff(const mpde_problem* prob, const mpde_template* t, const float* theta,
+                        const float* feat, float* coeff, float* rhs_b, mpde_stream_t stream);
+
+/* Device workspace bytes mpde_template_grad needs (fp64 partial sums of grad_theta). */
+size_t mpde_template_workspace_bytes(const mpde_problem* prob, const mpde_template* t);
+
+/* Chain rule through the template: from grad_coeff = dl/dc and grad_rhs = dl/db (e.g. the
+ * outputs of mpde_solve_bwd) writes grad_theta = dl/dtheta summed over the batch
+ * (deterministic fixed-order fp64 reduction) and, if grad_feat != NULL, dl/du~ per PDE
+ * (the contribution through c and b only). */
+int mpde_template_grad(const mpde_problem* prob, const mpde_template* t, const float* theta,
+                       const float* feat, const float* grad_coeff, const float* grad_rhs,
+                       float* grad_theta, float* grad_feat, void* workspace,
+                       size_t workspace_bytes, mpde_stream_t stream);
+
 /* ---- launch profiler (process-wide, not thread-safe; off by default) ------------
  * Between begin and end every library launch is bracketed by CUDA events on the
  * stream it is launched on.  end() synchronises and returns, per launch class,

@@ -148,5 +148,15 @@ void launch_fwd_out(const Geo& G, int B, const float* c, const float* b, const d
 void launch_d2f(size_t n, const double* a, float* b, cudaStream_t s);
 void launch_batch_sum(const float* x, int B, int64_t n, float* out, cudaStream_t s);
 void launch_stats_out(int B, const PdeState& st, mpde_stats* out, cudaStream_t s);
+// template.cu: polynomial PDE-expression template (mpde_template_*)
+constexpr int kTmplMaxK = 35;  // C(3+4, 4): 3 feature fields, degree 4
+constexpr int kTmplMaxR = 8;   // |M| + 1 in 3D
+int template_terms(int F, int G);  // K, or -1 if (F, G) is outside 1..3 x 0..4
+size_t template_partials(int P, int B, int F, int G, int M);  // fp64 partials of grad_theta
+cudaError_t launch_template_coeff(int P, int B, int M, int F, int G, const float* theta,
+                                  const float* feat, float* coeff, float* rhs, cudaStream_t s);
+cudaError_t launch_template_grad(int P, int B, int M, int F, int G, const float* theta,
+                                 const float* feat, const float* gc, const float* gb,
+                                 float* gtheta, float* gfeat, double* part, cudaStream_t s);
 
 }  // namespace mpde

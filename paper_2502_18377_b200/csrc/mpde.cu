@@ -1058,6 +1058,61 @@ int mpde_batch_sum(const float* x, int32_t batch, int64_t n, float* out, mpde_st
   return MPDE_OK;
 }
 
+int32_t mpde_template_terms(const mpde_template* t) {
+  return t ? template_terms(t->n_feat, t->degree) : -1;
+}
+
+static int template_check(const mpde_problem* prob, const mpde_template* t) {
+  mpde_options o = mpde_default_options();
+  if (int rc = validate(prob, &o)) return rc;
+  if (!t) return set_err(MPDE_ERR_INVALID_ARG, "null template");
+  if (template_terms(t->n_feat, t->degree) < 0)
+    return set_err(MPDE_ERR_UNSUPPORTED, "template needs n_feat in 1..3 and degree in 0..4 (got %d, %d)",
+                   t->n_feat, t->degree);
+  return MPDE_OK;
+}
+
+int mpde_template_coeff(const mpde_problem* prob, const mpde_template* t, const float* theta,
+                        const float* feat, float* coeff, float* rhs_b, mpde_stream_t stream_) {
+  if (int rc = template_check(prob, t)) return rc;
+  if (!theta || !feat || !coeff || !rhs_b) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  int P = 1;
+  for (int d = 0; d < prob->ndim; ++d) P *= prob->n[d];
+  const cudaError_t e = launch_template_coeff(P, prob->batch, 1 + 2 * prob->ndim, t->n_feat,
+                                              t->degree, theta, feat, coeff, rhs_b,
+                                              (cudaStream_t)stream_);
+  if (e != cudaSuccess) return set_err(MPDE_ERR_CUDA, "template_coeff: %s", cudaGetErrorString(e));
+  return MPDE_OK;
+}
+
+size_t mpde_template_workspace_bytes(const mpde_problem* prob, const mpde_template* t) {
+  if (template_check(prob, t)) return 0;
+  int P = 1;
+  for (int d = 0; d < prob->ndim; ++d) P *= prob->n[d];
+  return sizeof(double) *
+         template_partials(P, prob->batch, t->n_feat, t->degree, 1 + 2 * prob->ndim);
+}
+
+int mpde_template_grad(const mpde_problem* prob, const mpde_template* t, const float* theta,
+                       const float* feat, const float* grad_coeff, const float* grad_rhs,
+                       float* grad_theta, float* grad_feat, void* workspace,
+                       size_t workspace_bytes, mpde_stream_t stream_) {
+  if (int rc = template_check(prob, t)) return rc;
+  if (!theta || !feat || !grad_coeff || !grad_rhs || !grad_theta || !workspace)
+    return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  if (workspace_bytes < mpde_template_workspace_bytes(prob, t))
+    return set_err(MPDE_ERR_WORKSPACE, "template workspace %zu < %zu bytes", workspace_bytes,
+                   mpde_template_workspace_bytes(prob, t));
+  int P = 1;
+  for (int d = 0; d < prob->ndim; ++d) P *= prob->n[d];
+  const cudaError_t e = launch_template_grad(P, prob->batch, 1 + 2 * prob->ndim, t->n_feat,
+                                             t->degree, theta, feat, grad_coeff, grad_rhs,
+                                             grad_theta, grad_feat, (double*)workspace,
+                                             (cudaStream_t)stream_);
+  if (e != cudaSuccess) return set_err(MPDE_ERR_CUDA, "template_grad: %s", cudaGetErrorString(e));
+  return MPDE_OK;
+}
+
 size_t mpde_host_staging_bytes(const mpde_problem* prob) {
   mpde_options o = mpde_default_options();
   if (validate(prob, &o)) return 0;

@@ -40,6 +40,10 @@ class mpde_stats(C.Structure):
                 ("rel_res", C.c_float), ("err_est", C.c_float)]
 
 
+class mpde_template(C.Structure):
+    _fields_ = [("n_feat", C.c_int32), ("degree", C.c_int32)]
+
+
 STATUS = {0: "converged", 1: "maxiter", 2: "nonfinite", 3: "indefinite"}
 _lib = None
 
@@ -74,6 +78,13 @@ def lib():
         L.mpde_host_staging_bytes.restype = C.c_size_t
         L.mpde_fwd_bwd_host.argtypes = [P, O, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                         C.c_size_t, S]
+        T = C.POINTER(mpde_template)
+        L.mpde_template_terms.argtypes = [T]
+        L.mpde_template_terms.restype = C.c_int32
+        L.mpde_template_coeff.argtypes = [P, T, vp, vp, vp, vp, S]
+        L.mpde_template_workspace_bytes.argtypes = [P, T]
+        L.mpde_template_workspace_bytes.restype = C.c_size_t
+        L.mpde_template_grad.argtypes = [P, T, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, S]
         _lib = L
     return _lib
 
@@ -82,7 +93,8 @@ EXPORTS = ["mpde_default_options", "mpde_sizes", "mpde_workspace_bytes", "mpde_b
            "mpde_solve_fwd", "mpde_solve_bwd", "mpde_destroy_hierarchy", "mpde_last_error",
            "mpde_apply_normal", "mpde_apply_schur", "mpde_apply_precond", "mpde_hierarchy_query",
            "mpde_host_staging_bytes", "mpde_fwd_bwd_host", "mpde_batch_sum",
-           "mpde_profile_begin", "mpde_profile_end", "mpde_launch_count"]
+           "mpde_profile_begin", "mpde_profile_end", "mpde_launch_count", "mpde_template_terms",
+           "mpde_template_coeff", "mpde_template_workspace_bytes", "mpde_template_grad"]
 PROF_CLASSES = ["schur_g", "schur_out", "residual64", "condense", "backsub", "transfer",
                 "vector", "scalar", "coarse", "build", "epilogue", "schur_out_l0", "schur_g_l0"]
 
@@ -222,6 +234,39 @@ def mpde_fwd_bwd_host(prob, opts, c_h, b_h, om_h, g_h, z_h, gc_h, gb_h, gw_h, st
                                    _ptr(g_h), _ptr(z_h), _ptr(gc_h), _ptr(gb_h), _ptr(gw_h),
                                    _ptr(staging), _ptr(workspace), workspace.numel(),
                                    _stream(stream)))
+
+
+def make_template(n_feat, degree):
+    t = mpde_template()
+    t.n_feat, t.degree = int(n_feat), int(degree)
+    return t
+
+
+def mpde_template_terms(tmpl):
+    return int(lib().mpde_template_terms(C.byref(tmpl)))
+
+
+def mpde_template_coeff(prob, tmpl, theta, feat, coeff, rhs_b, stream=None):
+    """theta [|M|+1][K], feat [B][F][P] -> coeff [B][|M|][P], rhs_b [B][P] (all CUDA fp32)."""
+    _check(lib().mpde_template_coeff(C.byref(prob), C.byref(tmpl), _ptr(_dev_f32(theta, "theta")),
+                                     _ptr(_dev_f32(feat, "feat")), _ptr(_dev_f32(coeff, "coeff")),
+                                     _ptr(_dev_f32(rhs_b, "rhs_b")), _stream(stream)))
+
+
+def mpde_template_workspace_bytes(prob, tmpl):
+    n = lib().mpde_template_workspace_bytes(C.byref(prob), C.byref(tmpl))
+    if n == 0:
+        raise RuntimeError("invalid problem/template")
+    return n
+
+
+def mpde_template_grad(prob, tmpl, theta, feat, grad_coeff, grad_rhs, grad_theta, grad_feat,
+                       workspace, stream=None):
+    _check(lib().mpde_template_grad(C.byref(prob), C.byref(tmpl), _ptr(theta), _ptr(feat),
+                                    _ptr(_dev_f32(grad_coeff, "grad_coeff")),
+                                    _ptr(_dev_f32(grad_rhs, "grad_rhs")),
+                                    _ptr(_dev_f32(grad_theta, "grad_theta")), _ptr(grad_feat),
+                                    _ptr(workspace), workspace.numel(), _stream(stream)))
 
 
 # ------------------------------------------------------------------------------------

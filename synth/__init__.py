@@ -6,5 +6,5 @@ values omega and loss directions g shaped like the paper's workloads, rounded on
 to float32.  See DESIGN.md "Input recipe" and SURVEY.md §8(d).
 """
 from .gen import (  # noqa: F401
-    CONFIGS, Config, make_batch, make_pde, make_mms, make_g, field_names,
+    CONFIGS, Config, make_batch, make_pde, make_mms, make_g, field_names, make_template_batch,
 )

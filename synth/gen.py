@@ -228,3 +228,22 @@ def make_g(cfg_name: str, batch: int | None = None, start: int = 0, seed: int = 
         rng = np.random.default_rng(seed * 100_000 + 1000 * cfg.k + start + i)
         out[i] = rng.standard_normal((1 + 2 * D, P))
     return out
+
+
+def make_template_batch(cfg_name: str, batch: int | None = None, start: int = 0):
+    """Template twin of the C4 Navier-Stokes workload (SURVEY.md §8(f) N2, P:551-553:
+    "degree 1 polynomials"): feature fields u~ = (U1, U2) [B][2][P] and the parameters
+    theta [|M|+1][3] (monomials 1, U1, U2) of the vorticity-transport equation the C4
+    generator draws: c_t = 1, c_x = U1, c_y = U2, c_xx = c_yy = -nu, b = 0.  Only draws
+    inputs; evaluating the template is the method's job."""
+    if CONFIGS[cfg_name].kind != "ns2d":
+        raise ValueError("template twin defined for the NS-vorticity configs (C4, C5)")
+    bt = make_batch(cfg_name, batch, start)
+    feat = np.ascontiguousarray(bt["c"][:, [3, 5]])
+    nu = np.float32(1e-3)
+    theta = np.zeros((8, 3), np.float32)
+    theta[1, 0] = 1.0
+    theta[3, 1] = 1.0
+    theta[5, 2] = 1.0
+    theta[4, 0] = theta[6, 0] = -nu
+    return {"cfg": bt["cfg"], "feat": feat, "theta": theta, "omega": bt["omega"], "c": bt["c"]}

@@ -71,3 +71,21 @@ def test_workspace_scales_linearly_in_batch(mp):
     assert 30 * w1 < w32 < 33 * w1
     # ~ tens of bytes per unknown (matrix-free), far below a CSR A^T A
     assert w32 / (32 * 7 * 131072) < 80
+
+
+def test_template_terms_and_validation(mp):
+    """mpde_template_terms = C(F+G, G) (the oracle's monomial count); unsupported templates
+    are refused synchronously."""
+    from math import comb
+
+    from oracle.template import monomials
+    for F in (1, 2, 3):
+        for G in range(5):
+            assert mp.mpde_template_terms(mp.make_template(F, G)) == comb(F + G, G) \
+                == len(monomials(F, G))
+    assert mp.mpde_template_terms(mp.make_template(4, 1)) == -1
+    assert mp.mpde_template_terms(mp.make_template(1, 5)) == -1
+    pr = mp.make_problem((32, 64, 64), (0.01, 1 / 64, 1 / 64), 32)
+    # fp64 partials of grad_theta: one per (PDE, CTA of 1024 points) and (|M|+1) K entries
+    assert mp.mpde_template_workspace_bytes(pr, mp.make_template(2, 1)) == 8 * 32 * 128 * 8 * 3
+    assert mp.lib().mpde_template_workspace_bytes(C.byref(pr), C.byref(mp.make_template(2, 7))) == 0
