@@ -311,6 +311,46 @@ def run_ours(a):
         e2e = {"value": world * B * ke / (te_ms / 1e3), "unit": "PDE solves/s (fwd+bwd)",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
+    # ---- the paper's discovery step: polynomial template -> solve -> dl/dtheta -> all-reduce
+    tstep = None
+    if not a.no_template:
+        from paper_2502_18377_b200.parallel import allreduce_theta_grad
+        tm = mpde.make_template(2, 1)
+        theta = torch.from_numpy(synth.ns_template_theta()).to(dev)
+        feats = [torch.from_numpy(np.ascontiguousarray(s["np"][0][:, [3, 5]])).to(dev) for s in sets]
+        ct = torch.empty((B, M, P), dtype=torch.float32, device=dev)
+        bt_ = torch.empty((B, P), dtype=torch.float32, device=dev)
+        gth = torch.empty_like(theta)
+        tws = torch.empty(mpde.mpde_template_workspace_bytes(prob, tm), dtype=torch.uint8, device=dev)
+
+        def tstep_fn(i):
+            s = sets[i % 2]
+            mpde.mpde_template_coeff(prob, tm, theta, feats[i % 2], ct, bt_, stream)
+            h = mpde.mpde_build_hierarchy(prob, opts, ct, ws, stream)
+            mpde.mpde_solve_fwd(h, bt_, s["om"], z, stats_f, stream)
+            mpde.mpde_solve_bwd(h, bt_, z, s["g"], gc, gb, gw, None, stats_b, stream)
+            mpde.mpde_template_grad(prob, tm, theta, feats[i % 2], gc, gb, gth, None, tws, stream)
+            allreduce_theta_grad(gth)  # NCCL: the shared-parameter gradient (a few hundred bytes)
+            mpde.mpde_destroy_hierarchy(h)
+
+        for i in range(a.warmup):
+            tstep_fn(i)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0e.record(stream)
+        for i in range(a.steps):
+            tstep_fn(i)
+        t1e.record(stream)
+        torch.cuda.synchronize()
+        tms = max_over_ranks(t0e.elapsed_time(t1e), device=dev)
+        tstep = {"value": world * B * a.steps / (tms / 1e3), "unit": "PDE solves/s (fwd+bwd)",
+                 "ms_per_step": tms / a.steps,
+                 "workload": "C4 as a discovery step: degree-1 template in (U1, U2) (P:552) -> "
+                             "build -> fwd -> bwd -> dl/dtheta -> all-reduce of [8][3] fp32",
+                 "allreduce_bytes": gth.numel() * 4}
+
     if rank == 0:
         cpu = None
         if world == 1 and not a.no_cpu:
@@ -345,6 +385,7 @@ def run_ours(a):
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "template_step": tstep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -388,6 +429,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-template", action="store_true")
     a = ap.parse_args()
     if a.impl == "reference":
         run_reference(a)

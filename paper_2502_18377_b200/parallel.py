@@ -28,6 +28,13 @@ def allreduce_coeff_grad(gsum_local: torch.Tensor, group=None) -> torch.Tensor:
     return gsum_local
 
 
+def allreduce_theta_grad(grad_theta: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place SUM all-reduce of the template-parameter gradient [|M|+1][K] (a few hundred
+    bytes): the collective of the paper's data-parallel discovery step, where theta is
+    shared by every PDE of the global batch."""
+    return allreduce_coeff_grad(grad_theta, group)
+
+
 def max_over_ranks(x: float, device=None, group=None) -> float:
     """Max of a host scalar over ranks (device time of the slowest rank)."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:

@@ -7,4 +7,5 @@ to float32.  See DESIGN.md "Input recipe" and SURVEY.md §8(d).
 """
 from .gen import (  # noqa: F401
     CONFIGS, Config, make_batch, make_pde, make_mms, make_g, field_names, make_template_batch,
+    ns_template_theta,
 )

@@ -240,10 +240,17 @@ def make_template_batch(cfg_name: str, batch: int | None = None, start: int = 0)
         raise ValueError("template twin defined for the NS-vorticity configs (C4, C5)")
     bt = make_batch(cfg_name, batch, start)
     feat = np.ascontiguousarray(bt["c"][:, [3, 5]])
+    return {"cfg": bt["cfg"], "feat": feat, "theta": ns_template_theta(), "omega": bt["omega"],
+            "c": bt["c"]}
+
+
+def ns_template_theta():
+    """theta [8][3] of the NS template twin (monomials 1, U1, U2; rows phi, t, tt, x, xx, y,
+    yy, b): c_t = 1, c_x = U1, c_y = U2, c_xx = c_yy = -nu (nu = 1e-3, P:442), b = 0."""
     nu = np.float32(1e-3)
     theta = np.zeros((8, 3), np.float32)
     theta[1, 0] = 1.0
     theta[3, 1] = 1.0
     theta[5, 2] = 1.0
     theta[4, 0] = theta[6, 0] = -nu
-    return {"cfg": bt["cfg"], "feat": feat, "theta": theta, "omega": bt["omega"], "c": bt["c"]}
+    return theta
