@@ -100,6 +100,10 @@ typedef struct {
   float   tol_z;      /* error-based stop: after >= 2 refinement passes, stop when the
                          estimate ||d_k||^2/||d_k-1|| / ||z|| <= tol_z (d_k = correction of
                          pass k); `tol` above is a residual floor that also stops        */
+  float   tol_inner2; /* PCG stop for refinement passes >= 2: ||r_k|| / ||r_0|| <= tol_inner2.
+                         The first pass must reach tol_inner; later passes only correct it,
+                         and the error estimate of pass k >= 2 is ||d_k|| * max(||d_k|| /
+                         ||d_k-1||, tol_inner2) / ||z|| (Q14)                    */
 } mpde_options;
 
 /* one per PDE, device memory, written by mpde_solve_fwd / mpde_solve_bwd */
@@ -113,7 +117,7 @@ typedef struct {
 
 typedef struct mpde_hierarchy mpde_hierarchy; /* opaque, host-side handle */
 
-/* Defaults: tol_z 1e-4 (measured errors 10-100x below it on C2-C4 and their MMS twins), tol 1e-10, tol_inner 3e-4, max_refine 6, Chebyshev nu = 2, coarsest 8,
+/* Defaults: tol_z 1e-4 (measured errors 4-100x below it on C2-C4 and their MMS twins), tol 1e-10, tol_inner 3e-4, tol_inner2 3e-3, max_refine 6, Chebyshev nu = 2, coarsest 8,
  * 16 Lanczos steps, precision 1. */
 mpde_options mpde_default_options(void);
 

@@ -73,6 +73,7 @@ struct PdeState {
   double* errest;  // estimated relative error of z after the last pass
   float tol;       // residual floor (stop when ||A^T(d-Az)||/||A^T d|| <= tol)
   float tol_z;     // error-based stop (estimated ||z - z*|| / ||z|| <= tol_z)
+  float tol2_later;  // (PCG relative tolerance of refinement passes >= 2)^2
 };
 
 int ntiles(int P);

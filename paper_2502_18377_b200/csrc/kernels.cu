@@ -654,8 +654,11 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
     double S2 = 0.0;  // ||z||^2 partials live in the second half of part
     for (int t = 0; t < nt; ++t) S2 += part[(size_t)B * nt + (size_t)v * nt + t];
     const double dz = sqrt(S_), zn = sqrt(S2);
-    // geometric refinement: err_k ~ ||d_k|| * (||d_k|| / ||d_{k-1}||)
-    const double est = st.refines[v] >= 2 && st.dzprev[v] > 0 ? dz * (dz / st.dzprev[v]) : dz;
+    // geometric refinement: err_k ~ ||d_k|| * rho_k with rho_k the larger of the observed
+    // contraction ||d_k|| / ||d_{k-1}|| and the relative tolerance pass k was solved to
+    const double est = st.refines[v] >= 2 && st.dzprev[v] > 0
+                           ? dz * fmax(dz / st.dzprev[v], sqrt((double)st.tol2_later))
+                           : dz;
     st.dzprev[v] = dz;
     st.errest[v] = zn > 0 ? est / zn : (dz > 0 ? 1.0 : 0.0);
     return;
@@ -740,7 +743,8 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
     st.pass_iters[v] += 1;
     if (!isfinite(rr)) {
       pcg_fail(st, v, rr);
-    } else if (rr <= (double)tol2 * st.rr0[v] || st.pass_iters[v] >= max_iters ||
+    } else if (rr <= (st.refines[v] >= 2 ? (double)st.tol2_later : (double)tol2) * st.rr0[v] ||
+               st.pass_iters[v] >= max_iters ||
                rr <= 0.25 * (double)st.tol * st.tol * st.rhsn[v] * st.rhsn[v]) {
       // pass finished: relative inner tolerance (the fp32 limit) reached, or the outer
       // target itself (after exact back-substitution the full normal residual equals the

@@ -88,7 +88,7 @@ int validate(const mpde_problem* pr, const mpde_options* op) {
     return set_err(MPDE_ERR_INVALID_ARG, "lanczos_steps must be in 2..32");
   if (op->precision < 0 || op->precision > 3)
     return set_err(MPDE_ERR_INVALID_ARG, "precision must be in 0..3");
-  if (!(op->tol > 0) || !(op->tol_inner > 0) || !(op->tol_z > 0))
+  if (!(op->tol > 0) || !(op->tol_inner > 0) || !(op->tol_z > 0) || !(op->tol_inner2 > 0))
     return set_err(MPDE_ERR_INVALID_ARG, "tolerances must be > 0");
   return MPDE_OK;
 }
@@ -750,6 +750,7 @@ mpde_options mpde_default_options(void) {
   o.lanczos_steps = 16;
   o.precision = 1;
   o.use_graphs = 1;
+  o.tol_inner2 = 3e-3f;  // tools/calib_tol.py: -16% iterations on C4, e_z <= 2.7e-5 on C2-C4
   return o;
 }
 
@@ -823,6 +824,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
   }
   h->st.tol = opts->tol;
   h->st.tol_z = opts->tol_z;
+  h->st.tol2_later = opts->tol_inner2 * opts->tol_inner2;
   const int B = h->B, M = h->M, L = h->L;
   g_launch_count += 2;
   k_fill_int<<<(B + 255) / 256, 256, 0, s>>>(B, h->ones, 1);
