@@ -20,6 +20,9 @@
 #include <mutex>
 #include <vector>
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "internal.h"
 
 using namespace mpde;
@@ -449,21 +452,42 @@ PdeState state_with_lmax(const mpde_hierarchy* h, double* lmax) {
 // precision tiers (mpde_options.precision): f64 arithmetic for the PCG operator and
 // the condensation when >= 1, for the V-cycle too when >= 2 (f64_outer / f64_vcycle).
 
+// EXPERIMENT (env MPDE_CF_EMU = 1 fp16, 2 bf16): the level-0 smoother / residual applies of
+// the V-cycle use S built from rounded per-point coefficients (still symmetric PSD: only the
+// preconditioner changes); the PCG operator keeps the fp32 coefficients.
+static int cf_emu_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("MPDE_CF_EMU");
+    m = e ? atoi(e) : 0;
+  }
+  return m;
+}
+static float* g_cfemu = nullptr;
+static size_t g_cfemu_n = 0;
+__global__ void k_round_cf(size_t n, int mode, const float* __restrict__ x, float* __restrict__ y) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  y[i] = mode == 1 ? __half2float(__float2half(x[i])) : __bfloat162float(__float2bfloat16(x[i]));
+}
+
 int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const float* x,
                 const EpiArgs& A, const int* act, bool f64, cudaStream_t s) {
   Level& lv = h->lv[l];
+  const float* cf = lv.cf;
+  if (l == 0 && g_cfemu && epi != EPI_DOT && epi != EPI_STORE && epi != EPI_POWER) cf = g_cfemu;
   EpiArgs A2 = A;
   // profiling: level 0 has its own classes (11 pass 2, 12 pass 1) and point counters
   A2.pts = g_prof.on ? g_prof.d_pts + (l == 0 ? 9 : 0) : nullptr;
   const int c_out = l == 0 ? 11 : 1, c_g = l == 0 ? 12 : 0;
   if (schur_fused(lv.G, f64)) {
-    PROF(c_out, s, launch_schur_fused(epi, lv.G, nvec, crep, lv.cf, x, A2, act, s));
+    PROF(c_out, s, launch_schur_fused(epi, lv.G, nvec, crep, cf, x, A2, act, s));
     CKL();
     return MPDE_OK;
   }
-  PROF(c_g, s, launch_schur_g(lv.G, nvec, crep, lv.cf, x, lv.g, act,
+  PROF(c_g, s, launch_schur_g(lv.G, nvec, crep, cf, x, lv.g, act,
                               g_prof.on ? g_prof.d_pts + (l == 0 ? 7 : 8) : nullptr, f64, s));
-  PROF(c_out, s, launch_schur_out(epi, lv.G, nvec, crep, lv.cf, x, lv.g, A2, act, f64, s));
+  PROF(c_out, s, launch_schur_out(epi, lv.G, nvec, crep, cf, x, lv.g, A2, act, f64, s));
   CKL();
   return MPDE_OK;
 }
@@ -858,6 +882,16 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
     }
     launch_schur_coef(lv.G, B, lv.c, lv.cf, s);
     launch_diag_schur(lv.G, B, lv.cf, lv.dinv, s);
+    if (l == 0 && cf_emu_mode()) {
+      const size_t n = (size_t)B * (2 + 2 * h->prob.ndim) * lv.P;
+      if (g_cfemu_n < n) {
+        if (g_cfemu) cudaFree(g_cfemu);
+        CK(cudaMalloc(&g_cfemu, n * sizeof(float)));
+        g_cfemu_n = n;
+      }
+      ++g_launch_count;
+      k_round_cf<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, cf_emu_mode(), lv.cf, g_cfemu);
+    }
     CKL();
     if (l == L - 1) break;
     // lambda_max(D^-1 S) per PDE: Lanczos in the D-inner product (D = diag S), then the

@@ -17,6 +17,8 @@ B = 4
 settings = [dict(tol_inner2=3e-4), dict(tol_inner2=3e-3), dict(tol_inner2=1e-2),
             dict(tol_inner2=3e-2), dict(tol_inner2=1e-1), dict(tol_inner=1e-3, tol_inner2=1e-2),
             dict(tol_inner=1e-4, tol_inner2=1e-2), dict(tol_inner=1e-4, tol_inner2=3e-2)]
+if len(sys.argv) > 2 and sys.argv[2] == "default":
+    settings = [dict()]
 bt = synth.make_batch(name, batch=B)
 g = synth.make_g(name, batch=B)
 mm = synth.make_mms(name, batch=B)
