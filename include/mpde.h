@@ -104,6 +104,10 @@ typedef struct {
                          The first pass must reach tol_inner; later passes only correct it,
                          and the error estimate of pass k >= 2 is ||d_k|| * max(||d_k|| /
                          ||d_k-1||, tol_inner2) / ||z|| (Q14)                    */
+  int32_t cf_bf16;    /* 1 = the V-cycle's level-0 S applies read the per-point coefficients
+                         of S as bf16 (half the bytes); S~ stays symmetric PSD, so the
+                         preconditioner is still a fixed SPD map.  The PCG operator, the
+                         refinement residual and the gradients keep fp32 / fp64 (default 1) */
 } mpde_options;
 
 /* one per PDE, device memory, written by mpde_solve_fwd / mpde_solve_bwd */

@@ -108,6 +108,15 @@ bool schur_fused(const Geo& G, bool f64);
 void launch_schur_fused(int epi, const Geo& G, int nvec, int crep, const float* cf,
                         const float* x, const EpiArgs& A, const int* act, cudaStream_t s);
 void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaStream_t s);
+// bf16 per-point coefficients (cf16: [B][2+2D][P] __nv_bfloat16) for the V-cycle's applies
+// (epilogues RESID / SMOOTH / SMOOTH_LAST / POST0); only where schur_bf16_ok()
+bool schur_bf16_ok(const Geo& G, bool f64);
+void launch_schur_g_bf(const Geo& G, int nvec, int crep, const void* cf16, const float* x, void* g,
+                       const int* act, unsigned long long* pts, cudaStream_t s);
+void launch_schur_out_bf(int epi, const Geo& G, int nvec, int crep, const void* cf16,
+                         const float* x, const void* g, const EpiArgs& A, const int* act,
+                         cudaStream_t s);
+void launch_f2bf(size_t n, const float* a, void* b, cudaStream_t s);
 void launch_restrict(const Geo& Gf, const Geo& Gc, int nvec, int nfield, const float* fine,
                      float* coarse, const int* act, int crep, cudaStream_t s);
 void launch_prolong(const Geo& Gf, const Geo& Gc, int nvec, const float* coarse, float* fine,

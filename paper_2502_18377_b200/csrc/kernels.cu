@@ -16,6 +16,8 @@
 // v / crep (crep > 1 only for the coarsest-level probing).  act[pde] == 0 skips the
 // whole CTA (converged / failed PDEs).
 #include "common.cuh"
+#include <cuda_bf16.h>
+
 #include "internal.h"
 
 namespace mpde {
@@ -883,6 +885,12 @@ __global__ void __launch_bounds__(kThreads) k_batch_sum(const float* __restrict_
   out[j] = float(acc);
 }
 
+__global__ void __launch_bounds__(kThreads) k_f2bf(size_t n, const float* __restrict__ a,
+                                                   __nv_bfloat16* __restrict__ b) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = __float2bfloat16_rn(a[i]);
+}
+
 __global__ void __launch_bounds__(kThreads) k_d2f(size_t n, const double* __restrict__ a, float* __restrict__ b) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = float(a[i]);
@@ -1056,6 +1064,10 @@ void launch_fwd_out(const Geo& G, int B, const float* c, const float* b, const d
 void launch_batch_sum(const float* x, int B, int64_t n, float* out, cudaStream_t s) {
   ++g_launch_count;
   k_batch_sum<<<(unsigned)((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(x, B, n, out);
+}
+void launch_f2bf(size_t n, const float* a, void* b, cudaStream_t s) {
+  ++g_launch_count;
+  k_f2bf<<<(unsigned)((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(n, a, (__nv_bfloat16*)b);
 }
 void launch_d2f(size_t n, const double* a, float* b, cudaStream_t s) {
   ++g_launch_count;

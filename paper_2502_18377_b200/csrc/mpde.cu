@@ -20,9 +20,6 @@
 #include <mutex>
 #include <vector>
 
-#include <cuda_bf16.h>
-#include <cuda_fp16.h>
-
 #include "internal.h"
 
 using namespace mpde;
@@ -84,6 +81,8 @@ int validate(const mpde_problem* pr, const mpde_options* op) {
     return set_err(MPDE_ERR_INVALID_ARG, "row-group weights must be > 0");
   if (op->smoother < 0 || op->smoother > 1)
     return set_err(MPDE_ERR_UNSUPPORTED, "smoother must be 0 (Jacobi) or 1 (Chebyshev)");
+  if (op->cf_bf16 != 0 && op->cf_bf16 != 1)
+    return set_err(MPDE_ERR_INVALID_ARG, "cf_bf16 must be 0 or 1");
   if (op->nu < 1 || op->nu > 16) return set_err(MPDE_ERR_INVALID_ARG, "nu must be in 1..16");
   if (op->max_refine < 1 || op->max_iters < 1 || op->poll_every < 1)
     return set_err(MPDE_ERR_INVALID_ARG, "max_refine, max_iters, poll_every must be >= 1");
@@ -310,6 +309,7 @@ struct Level {
   float* rr = nullptr;  // W-cycle: restricted residual kept (levels >= 1)
   float* ew = nullptr;  // W-cycle: first coarse correction
   float* cf;        // [B][2+2D][P] per-point coefficients of S (schur.cu)
+  void* cf16 = nullptr;  // level 0, opts.cf_bf16: the same in bf16 for the V-cycle's applies
   float* tab;       // device row tables of S, sum_d n_d * kTabRow floats
   std::vector<float> tab_host;
 };
@@ -366,6 +366,7 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
     lv.P = shp[l].P;
     lv.cbuf = l > 0 ? bp.take<float>((size_t)B * M * lv.P) : nullptr;
     lv.cf = bp.take<float>((size_t)B * (2 + 2 * D) * lv.P);
+    lv.cf16 = (l == 0 && op->cf_bf16) ? bp.take<uint16_t>((size_t)B * (2 + 2 * D) * lv.P) : nullptr;
     {
       int off = 0;
       for (int d = 0; d < D; ++d) {
@@ -452,36 +453,29 @@ PdeState state_with_lmax(const mpde_hierarchy* h, double* lmax) {
 // precision tiers (mpde_options.precision): f64 arithmetic for the PCG operator and
 // the condensation when >= 1, for the V-cycle too when >= 2 (f64_outer / f64_vcycle).
 
-// EXPERIMENT (env MPDE_CF_EMU = 1 fp16, 2 bf16): the level-0 smoother / residual applies of
-// the V-cycle use S built from rounded per-point coefficients (still symmetric PSD: only the
-// preconditioner changes); the PCG operator keeps the fp32 coefficients.
-static int cf_emu_mode() {
-  static int m = -1;
-  if (m < 0) {
-    const char* e = getenv("MPDE_CF_EMU");
-    m = e ? atoi(e) : 0;
-  }
-  return m;
-}
-static float* g_cfemu = nullptr;
-static size_t g_cfemu_n = 0;
-__global__ void k_round_cf(size_t n, int mode, const float* __restrict__ x, float* __restrict__ y) {
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  y[i] = mode == 1 ? __half2float(__float2half(x[i])) : __bfloat162float(__float2bfloat16(x[i]));
-}
-
 int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const float* x,
                 const EpiArgs& A, const int* act, bool f64, cudaStream_t s) {
   Level& lv = h->lv[l];
   const float* cf = lv.cf;
-  if (l == 0 && g_cfemu && epi != EPI_DOT && epi != EPI_STORE && epi != EPI_POWER) cf = g_cfemu;
   EpiArgs A2 = A;
   // profiling: level 0 has its own classes (11 pass 2, 12 pass 1) and point counters
   A2.pts = g_prof.on ? g_prof.d_pts + (l == 0 ? 9 : 0) : nullptr;
   const int c_out = l == 0 ? 11 : 1, c_g = l == 0 ? 12 : 0;
   if (schur_fused(lv.G, f64)) {
     PROF(c_out, s, launch_schur_fused(epi, lv.G, nvec, crep, cf, x, A2, act, s));
+    CKL();
+    return MPDE_OK;
+  }
+  // V-cycle applies on level 0 read the bf16 copy of cf (opts.cf_bf16): the smoother and the
+  // residual use S~ built from rounded coefficients -- still symmetric PSD (S = P0 + M s M^T
+  // for any coefficient values), so the preconditioner stays a fixed SPD map; the PCG
+  // operator (EPI_DOT) and the refinement keep the fp32 / fp64 coefficients.
+  if (lv.cf16 && !f64 && crep == 1 &&
+      (epi == EPI_RESID || epi == EPI_SMOOTH || epi == EPI_SMOOTH_LAST || epi == EPI_POST0) &&
+      schur_bf16_ok(lv.G, f64)) {
+    PROF(c_g, s, launch_schur_g_bf(lv.G, nvec, crep, lv.cf16, x, lv.g, act,
+                                   g_prof.on ? g_prof.d_pts + (l == 0 ? 7 : 8) : nullptr, s));
+    PROF(c_out, s, launch_schur_out_bf(epi, lv.G, nvec, crep, lv.cf16, x, lv.g, A2, act, s));
     CKL();
     return MPDE_OK;
   }
@@ -774,6 +768,7 @@ mpde_options mpde_default_options(void) {
   o.lanczos_steps = 16;
   o.precision = 1;
   o.use_graphs = 1;
+  o.cf_bf16 = 1;
   o.tol_inner2 = 3e-3f;  // tools/calib_tol.py: -16% iterations on C4, e_z <= 2.7e-5 on C2-C4
   return o;
 }
@@ -882,16 +877,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
     }
     launch_schur_coef(lv.G, B, lv.c, lv.cf, s);
     launch_diag_schur(lv.G, B, lv.cf, lv.dinv, s);
-    if (l == 0 && cf_emu_mode()) {
-      const size_t n = (size_t)B * (2 + 2 * h->prob.ndim) * lv.P;
-      if (g_cfemu_n < n) {
-        if (g_cfemu) cudaFree(g_cfemu);
-        CK(cudaMalloc(&g_cfemu, n * sizeof(float)));
-        g_cfemu_n = n;
-      }
-      ++g_launch_count;
-      k_round_cf<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, cf_emu_mode(), lv.cf, g_cfemu);
-    }
+    if (lv.cf16) launch_f2bf((size_t)B * (2 + 2 * h->prob.ndim) * lv.P, lv.cf, lv.cf16, s);
     CKL();
     if (l == L - 1) break;
     // lambda_max(D^-1 S) per PDE: Lanczos in the D-inner product (D = diag S), then the

@@ -15,6 +15,8 @@
 //   [40,51) P0[o]     coefficient of x(i+o) in (P0 x)(i),       o = -5..5
 // Per point the kernels read cf = [sigma alpha, 1/sigma, u~ (2D)] (2+2D floats).
 #include "common.cuh"
+#include <cuda_bf16.h>
+
 #include "internal.h"
 
 #include <cstdlib>
@@ -249,6 +251,14 @@ __global__ void __launch_bounds__(kThreads) k_schur_diag(Geo G, const float* __r
 // of the tables come from the constant bank (G.irow); edge rows from the global table.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+// per-point coefficients cf: fp32, or bf16 for the V-cycle's level-0 applies
+// (mpde_options.cf_bf16; 4 consecutive points = one 8-byte load, widened by shifts)
+__device__ __forceinline__ float4 ldc4(const float* p) { return ld4(p); }
+__device__ __forceinline__ float4 ldc4(const __nv_bfloat16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                     __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+}
 __device__ __forceinline__ void st4(float* p, const float* v) {
   *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
 }
@@ -318,13 +328,13 @@ __device__ __forceinline__ int block_points(int remap, int P, int nlast, int p0_
   return min(4 * (int)blockDim.x, P - p0_first);
 }
 
-template <int D, typename T>
-__device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__ cb,
+template <int D, typename T, typename CF>
+__device__ __forceinline__ void schur_h4(const Geo& G, const CF* __restrict__ cb,
                                          const float* __restrict__ xb, int p0, const int* idx,
                                          T* g, int ymode) {
   const int P = G.P;
   {
-    const float4 x0 = ld4(xb + p0), c0 = ld4(cb + p0);
+    const float4 x0 = ld4(xb + p0), c0 = ldc4(cb + p0);
 #pragma unroll
     for (int j = 0; j < 4; ++j) g[j] = T(F4(c0, j)) * T(F4(x0, j));
   }
@@ -359,7 +369,7 @@ __device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__
         }
       }
     }
-    const float4 ua = ld4(cb + (size_t)(2 + 2 * d) * P + p0), ub = ld4(cb + (size_t)(3 + 2 * d) * P + p0);
+    const float4 ua = ldc4(cb + (size_t)(2 + 2 * d) * P + p0), ub = ldc4(cb + (size_t)(3 + 2 * d) * P + p0);
 #pragma unroll
     for (int j = 0; j < 4; ++j) g[j] -= T(F4(ua, j)) * k1[j] + T(F4(ub, j)) * k2[j];
   }
@@ -376,7 +386,7 @@ __device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__
       w[4 + j] = F4(wm, j);
       w[8 + j] = F4(wr, j);
     }
-    const float4 ua = ld4(cb + (size_t)(2 + 2 * d) * P + p0), ub = ld4(cb + (size_t)(3 + 2 * d) * P + p0);
+    const float4 ua = ldc4(cb + (size_t)(2 + 2 * d) * P + p0), ub = ldc4(cb + (size_t)(3 + 2 * d) * P + p0);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int i = i0 + j;
@@ -401,21 +411,21 @@ __device__ __forceinline__ void schur_h4(const Geo& G, const float* __restrict__
     }
   }
   {
-    const float4 c1 = ld4(cb + P + p0);
+    const float4 c1 = ldc4(cb + P + p0);
 #pragma unroll
     for (int j = 0; j < 4; ++j) g[j] *= T(F4(c1, j));
   }
 }
 
-template <int D, typename T>
-__device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__ cb,
+template <int D, typename T, typename CF>
+__device__ __forceinline__ void schur_s4(const Geo& G, const CF* __restrict__ cb,
                                          const float* __restrict__ xb, const T* __restrict__ hb,
                                          int p0, const int* idx, T* acc, int ymode) {
   const int P = G.P;
   {
     T h0[4];
     ldT4<T>(hb + p0, h0);
-    const float4 c0 = ld4(cb + p0);
+    const float4 c0 = ldc4(cb + p0);
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] = T(F4(c0, j)) * h0[j];
     // boundary rows: faces of the non-last axes cover all 4 points; last-axis faces per point
@@ -433,8 +443,8 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
 #pragma unroll
   for (int d = 0; d < D - 1; ++d) {
     const int n = G.n[d], s = G.stride[d], i = idx[d];
-    const float* u1 = cb + (size_t)(2 + 2 * d) * P;
-    const float* u2 = cb + (size_t)(3 + 2 * d) * P;
+    const CF* u1 = cb + (size_t)(2 + 2 * d) * P;
+    const CF* u2 = cb + (size_t)(3 + 2 * d) * P;
     if (i >= 7 && i <= n - 8) {
 #pragma unroll
       for (int o = -4; o <= 4; ++o) {
@@ -446,7 +456,7 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
 #pragma unroll
       for (int o = -2; o <= 2; ++o) {
         const int q = p0 + o * s;
-        const float4 va = ld4(u1 + q), vb = ld4(u2 + q);
+        const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q);
         T hv[4];
         ldT4<T>(hb + q, hv);
         const T a = G.irow[d][10 + (o + 2) * 2], b = G.irow[d][10 + (o + 2) * 2 + 1];
@@ -473,7 +483,7 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
       for (int o = -4; o <= 4; ++o) {
         const int oc = o < olo ? olo : (o > ohi ? ohi : o);
         const int q = p0 + oc * s;
-        const float4 va = ld4(u1 + q), vb = ld4(u2 + q);
+        const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q);
         T hv[4];
         ldT4<T>(hb + q, hv);
         const T a = ktr[(o + 4) * 2], b = ktr[(o + 4) * 2 + 1];
@@ -485,8 +495,8 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
   {  // last axis: x window (i0-8 .. i0+11), u1/u2/h windows (i0-4 .. i0+7)
     constexpr int d = D - 1;
     const int n = G.n[d], i0 = idx[d];
-    const float* u1 = cb + (size_t)(2 + 2 * d) * P;
-    const float* u2 = cb + (size_t)(3 + 2 * d) * P;
+    const CF* u1 = cb + (size_t)(2 + 2 * d) * P;
+    const CF* u2 = cb + (size_t)(3 + 2 * d) * P;
     float xw[20];
     float aw[12], bw[12];
     T hw[12];
@@ -502,8 +512,8 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
     for (int k = 0; k < 3; ++k) {
       const int off = -4 + 4 * k;
       const bool ok = (i0 + off >= 0) && (i0 + off < n);
-      const float4 va = ok ? ld4(u1 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 vb = ok ? ld4(u2 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 va = ok ? ldc4(u1 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 vb = ok ? ldc4(u2 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
       T hv[4] = {0, 0, 0, 0};
       if (ok) ldT4<T>(hb + p0 + off, hv);
 #pragma unroll
@@ -541,8 +551,8 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const float* __restrict__
   }
 }
 
-template <int D, typename T>
-__global__ void __launch_bounds__(kThreads) k_schur_h_v4(Geo G, const float* __restrict__ cf, int crep,
+template <int D, typename T, typename CF = float>
+__global__ void __launch_bounds__(kThreads) k_schur_h_v4(Geo G, const CF* __restrict__ cf, int crep,
                                                         const float* __restrict__ x,
                                                         T* __restrict__ hout, const int* act,
                                                         unsigned long long* pts, int remap) {
@@ -562,12 +572,12 @@ __global__ void __launch_bounds__(kThreads) k_schur_h_v4(Geo G, const float* __r
   int idx[D];
   unravel<D>(G, p0, idx);
   T g[4];
-  schur_h4<D, T>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, p0, idx, g, ymode);
+  schur_h4<D, T, CF>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, p0, idx, g, ymode);
   stT4<T>(hout + (size_t)v * P + p0, g);
 }
 
-template <int D, int EPI, typename T>
-__global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const float* __restrict__ cf, int crep,
+template <int D, int EPI, typename T, typename CF = float>
+__global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const CF* __restrict__ cf, int crep,
                                                         const float* __restrict__ x,
                                                         const T* __restrict__ hb, EpiArgs A,
                                                         const int* act, int remap) {
@@ -587,7 +597,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const float* __r
     unravel<D>(G, p0, idx);
     const size_t o = (size_t)v * P + p0;
     T acc[4];
-    schur_s4<D, T>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, hb + (size_t)v * P, p0, idx,
+    schur_s4<D, T, CF>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, hb + (size_t)v * P, p0, idx,
                    acc, ymode);
     float q[4];
 #pragma unroll
@@ -680,14 +690,14 @@ __device__ __forceinline__ int dim_s(const Geo& G, int ax) {
   return ax == 0 ? ((NX && NY) ? NX * NY : G.stride[0]) : ax == 1 ? (NY ? NY : G.stride[1]) : 1;
 }
 
-template <int AX, int NX, int NY>  // accumulate the AX-axis (0 = t, 1 = x) terms of a 2-output pencil
-__device__ __forceinline__ void pencil2(const Geo& G, const float* __restrict__ cb,
+template <int AX, int NX, int NY, typename CF>  // accumulate the AX-axis (0 = t, 1 = x) terms of a 2-output pencil
+__device__ __forceinline__ void pencil2(const Geo& G, const CF* __restrict__ cb,
                                         const float* __restrict__ xb, const float* __restrict__ hb,
                                         int pbase, int i0, bool ok1, float* acc0, float* acc1) {
   // pbase: offset of output 0 (index i0 along AX); output 1 is at pbase + s (index i0+1)
   const int P = G.P, n = dim_n<NX, NY>(G, AX), s = dim_s<NX, NY>(G, AX);
-  const float* u1 = cb + (size_t)(2 + 2 * AX) * P;
-  const float* u2 = cb + (size_t)(3 + 2 * AX) * P;
+  const CF* u1 = cb + (size_t)(2 + 2 * AX) * P;
+  const CF* u2 = cb + (size_t)(3 + 2 * AX) * P;
   if (i0 >= 7 && i0 + 1 <= n - 8) {
 #pragma unroll
     for (int u = -4; u <= 5; ++u) {
@@ -703,7 +713,7 @@ __device__ __forceinline__ void pencil2(const Geo& G, const float* __restrict__ 
 #pragma unroll
     for (int u = -2; u <= 3; ++u) {
       const int q = pbase + u * s;
-      const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
+      const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q), hv = ld4(hb + q);
       const float a0 = u <= 2 ? G.irow[AX][10 + (u + 2) * 2] : 0.f;
       const float b0 = u <= 2 ? G.irow[AX][10 + (u + 2) * 2 + 1] : 0.f;
       const float a1 = u >= -1 ? G.irow[AX][10 + (u + 1) * 2] : 0.f;
@@ -744,7 +754,7 @@ __device__ __forceinline__ void pencil2(const Geo& G, const float* __restrict__ 
   for (int u = -4; u <= 5; ++u) {
     const int ic = min(max(i0 + u, 0), n - 1);
     const int q = pbase + (ic - i0) * s;
-    const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
+    const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q), hv = ld4(hb + q);
     const float a0 = u <= 4 ? kta[(u + 4) * 2] : 0.f;
     const float b0 = u <= 4 ? kta[(u + 4) * 2 + 1] : 0.f;
     const float a1 = u >= -3 ? m1 * ktb[(u + 3) * 2] : 0.f;
@@ -758,13 +768,13 @@ __device__ __forceinline__ void pencil2(const Geo& G, const float* __restrict__ 
 }
 
 // one-output version of pencil2 (single quad, AX-axis terms)
-template <int AX, int NX, int NY>
-__device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ cb,
+template <int AX, int NX, int NY, typename CF>
+__device__ __forceinline__ void pencil1(const Geo& G, const CF* __restrict__ cb,
                                         const float* __restrict__ xb, const float* __restrict__ hb,
                                         int p0, int i, float* acc) {
   const int P = G.P, n = dim_n<NX, NY>(G, AX), s = dim_s<NX, NY>(G, AX);
-  const float* u1 = cb + (size_t)(2 + 2 * AX) * P;
-  const float* u2 = cb + (size_t)(3 + 2 * AX) * P;
+  const CF* u1 = cb + (size_t)(2 + 2 * AX) * P;
+  const CF* u2 = cb + (size_t)(3 + 2 * AX) * P;
   if (i >= 7 && i <= n - 8) {
 #pragma unroll
     for (int o = -4; o <= 4; ++o) {
@@ -776,7 +786,7 @@ __device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ 
 #pragma unroll
     for (int o = -2; o <= 2; ++o) {
       const int q = p0 + o * s;
-      const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
+      const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q), hv = ld4(hb + q);
       const float a = G.irow[AX][10 + (o + 2) * 2], b = G.irow[AX][10 + (o + 2) * 2 + 1];
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[j] -= (a * F4(va, j) + b * F4(vb, j)) * F4(hv, j);
@@ -800,7 +810,7 @@ __device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ 
   for (int o = -4; o <= 4; ++o) {
     const int oc = o < olo ? olo : (o > ohi ? ohi : o);
     const int q = p0 + oc * s;
-    const float4 va = ld4(u1 + q), vb = ld4(u2 + q), hv = ld4(hb + q);
+    const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q), hv = ld4(hb + q);
     const float a = ktr[(o + 4) * 2], b = ktr[(o + 4) * 2 + 1];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] -= (a * F4(va, j) + b * F4(vb, j)) * F4(hv, j);
@@ -808,14 +818,14 @@ __device__ __forceinline__ void pencil1(const Geo& G, const float* __restrict__ 
 }
 
 // y-axis (contiguous) terms + own terms of one quad, as in schur_s4
-template <int NX, int NY>
-__device__ __forceinline__ void quad_y_own(const Geo& G, const float* __restrict__ cb,
+template <int NX, int NY, typename CF>
+__device__ __forceinline__ void quad_y_own(const Geo& G, const CF* __restrict__ cb,
                                            const float* __restrict__ xb,
                                            const float* __restrict__ hb, int p0, int t, int xr,
                                            float* acc, int ymode) {
   const int P = G.P, n = dim_n<NX, NY>(G, 2), i0 = p0 % n;
   {
-    const float4 h0 = ld4(hb + p0), c0 = ld4(cb + p0), x0 = ld4(xb + p0);
+    const float4 h0 = ld4(hb + p0), c0 = ldc4(cb + p0), x0 = ld4(xb + p0);
     const bool face = (t == 0) | (t == G.n[0] - 1) | (xr == 0) | (xr == dim_n<NX, NY>(G, 1) - 1);
     const float wb2 = G.wb * G.wb;
 #pragma unroll
@@ -824,8 +834,8 @@ __device__ __forceinline__ void quad_y_own(const Geo& G, const float* __restrict
       if (face || i0 + j == 0 || i0 + j == n - 1) acc[j] += wb2 * F4(x0, j);
     }
   }
-  const float* u1 = cb + (size_t)6 * P;
-  const float* u2 = cb + (size_t)7 * P;
+  const CF* u1 = cb + (size_t)6 * P;
+  const CF* u2 = cb + (size_t)7 * P;
   float xw[20], aw[12], bw[12], hw[12];
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
@@ -839,8 +849,8 @@ __device__ __forceinline__ void quad_y_own(const Geo& G, const float* __restrict
   for (int k = 0; k < 3; ++k) {
     const int off = -4 + 4 * k;
     const bool ok = (i0 + off >= 0) && (i0 + off < n);
-    const float4 va = ok ? ld4(u1 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 vb = ok ? ld4(u2 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 va = ok ? ldc4(u1 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 vb = ok ? ldc4(u2 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 hv = ok ? ld4(hb + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -945,8 +955,8 @@ __device__ __forceinline__ double quad_epilogue(const EpiArgs& A, int pde, size_
   return dot;
 }
 
-template <int EPI, int BX, int NX, int NY, int YP>
-__global__ void __launch_bounds__(kThreads, 3) k_schur_s_b22(Geo G, const float* __restrict__ cf, int crep,
+template <int EPI, int BX, int NX, int NY, int YP, typename CF = float>
+__global__ void __launch_bounds__(kThreads, 3) k_schur_s_b22(Geo G, const CF* __restrict__ cf, int crep,
                                                          const float* __restrict__ x,
                                                          const float* __restrict__ hb, EpiArgs A,
                                                          const int* act, int remap) {
@@ -969,7 +979,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_schur_s_b22(Geo G, const float*
   double dot = 0.0;
   int nq = 0;
   if (tp < NT2) {
-    const float* cb = cf + (size_t)pde * 8 * P;
+    const CF* cb = cf + (size_t)pde * 8 * P;
     const float* xb = x + (size_t)v * P;
     const float* hv = hb + (size_t)v * P;
     const int t0 = 2 * tp, x0 = BX ? 2 * xp : xp;
@@ -1966,6 +1976,65 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
     EPI_CASE2(EPI_POST0)
   }
 #undef EPI_CASE2
+}
+
+// ---- bf16-coefficient variants (V-cycle applies on level 0, mpde_options.cf_bf16) ----------
+bool schur_bf16_ok(const Geo& G, bool f64) {
+  return !f64 && use_v4(G) && !use_hy(G, f64) && !use_tile(G, f64) && !use_fused(G, f64) &&
+         !(use_b22(G, f64) && block_mode() == 2);
+}
+
+void launch_schur_g_bf(const Geo& G, int nvec, int crep, const void* cf16, const float* x, void* g,
+                       const int* act, unsigned long long* pts, cudaStream_t s) {
+  ++g_launch_count;
+  const __nv_bfloat16* cf = static_cast<const __nv_bfloat16*>(cf16);
+  const int th = v4_threads(G);
+  dim3 gr((G.P + 4 * th - 1) / (4 * th), nvec);
+  DISPATCH_D2(G.D, (k_schur_h_v4<DD, float, __nv_bfloat16><<<gr, th, 0, s>>>(G, cf, crep, x, (float*)g, act, pts, 0)));
+}
+
+void launch_schur_out_bf(int epi, const Geo& G, int nvec, int crep, const void* cf16, const float* x,
+                         const void* g, const EpiArgs& A, const int* act, cudaStream_t s) {
+  ++g_launch_count;
+  const __nv_bfloat16* cf = static_cast<const __nv_bfloat16*>(cf16);
+  const float* gf = static_cast<const float*>(g);
+  if (use_b22(G, false)) {
+    const dim3 gb(schur_tiles(G, false), nvec);
+    const int rm = use_remap(G) ? b22_tp(G) : 0;
+#define B22BF(E)                                                                                  \
+  case E:                                                                                         \
+    if (G.n[1] == 64 && G.n[2] == 64)                                                             \
+      k_schur_s_b22<E, 0, 64, 64, 0, __nv_bfloat16><<<gb, kThreads, 0, s>>>(G, cf, crep, x, gf, A, act, rm); \
+    else if (G.n[1] == 32 && G.n[2] == 32)                                                        \
+      k_schur_s_b22<E, 0, 32, 32, 0, __nv_bfloat16><<<gb, kThreads, 0, s>>>(G, cf, crep, x, gf, A, act, rm); \
+    else if (G.n[1] == 128 && G.n[2] == 128)                                                      \
+      k_schur_s_b22<E, 0, 128, 128, 0, __nv_bfloat16><<<gb, kThreads, 0, s>>>(G, cf, crep, x, gf, A, act, rm); \
+    else                                                                                          \
+      k_schur_s_b22<E, 0, 0, 0, 0, __nv_bfloat16><<<gb, kThreads, 0, s>>>(G, cf, crep, x, gf, A, act, rm); \
+    break;
+    switch (epi) {
+      B22BF(EPI_RESID)
+      B22BF(EPI_SMOOTH)
+      B22BF(EPI_SMOOTH_LAST)
+      B22BF(EPI_POST0)
+    }
+#undef B22BF
+    return;
+  }
+  const int rm = use_remap(G);
+  const int th = v4_threads(G);
+  dim3 gr(schur_tiles(G, false), nvec);
+#define V4BF(E)                                                                                   \
+  case E:                                                                                         \
+    DISPATCH_D2(G.D, (k_schur_s_v4<DD, E, float, __nv_bfloat16><<<gr, th, 0, s>>>(G, cf, crep, x, gf, A, act, rm))); \
+    break;
+  switch (epi) {
+    V4BF(EPI_RESID)
+    V4BF(EPI_SMOOTH)
+    V4BF(EPI_SMOOTH_LAST)
+    V4BF(EPI_POST0)
+  }
+#undef V4BF
 }
 
 void launch_schur_fused(int epi, const Geo& G, int nvec, int crep, const float* cf,

@@ -32,7 +32,8 @@ class mpde_options(C.Structure):
                 ("coarsest", C.c_int32), ("levels_max", C.c_int32), ("poll_every", C.c_int32),
                 ("jacobi_theta", C.c_float), ("cheb_ratio", C.c_float),
                 ("lanczos_steps", C.c_int32), ("precision", C.c_int32),
-                ("use_graphs", C.c_int32), ("tol_z", C.c_float), ("tol_inner2", C.c_float)]
+                ("use_graphs", C.c_int32), ("tol_z", C.c_float), ("tol_inner2", C.c_float),
+                ("cf_bf16", C.c_int32)]
 
 
 class mpde_stats(C.Structure):

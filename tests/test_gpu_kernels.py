@@ -104,7 +104,9 @@ def test_large_schur_matches_sparse(shape, h, env, tmp_path):
         assert np.linalg.norm(y[i] - ref) <= 1e-4 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("shape,h", [((16, 18, 20), (0.05, 0.06, 0.07)), ((20, 24), (0.05, 0.04))])
+@pytest.mark.parametrize("shape,h", [((16, 18, 20), (0.05, 0.06, 0.07)), ((20, 24), (0.05, 0.04)),
+                                     ((20, 32, 32), (0.05, 0.03, 0.03)),
+                                     ((64, 96), (0.05, 0.02))])
 def test_vcycle_symmetric_positive(shape, h):
     """The V-cycle is a fixed SPD linear map (needed by PCG): <Ma, b> = <a, Mb>, <Ma, a> > 0."""
     from paper_2502_18377_b200 import mpde

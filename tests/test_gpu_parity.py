@@ -167,13 +167,17 @@ def test_c2_sampled_parity(gu):
             assert gu.rel(out[k][i], bw[k]) <= E_G, k
 
 
-def test_options_do_not_change_the_answer(gu):
-    """P12: smoother, nu, number of levels change iteration counts, not z*."""
+@pytest.mark.parametrize("shape", [(16, 20, 24), (20, 32, 32)])
+def test_options_do_not_change_the_answer(shape, gu):
+    """P12: smoother, nu, number of levels, the bf16 V-cycle coefficients (cf_bf16; the
+    (20,32,32) level 0 runs the t-blocked pass-2 kernel) and the refinement tolerances change
+    iteration counts, not z*."""
     from paper_2502_18377_b200 import mpde
-    shape, h = (16, 20, 24), (0.05, 0.05, 0.05)
+    h = (0.05, 0.05, 0.05)
     c, b, om, _ = _rand_problem(shape, 2, 41)
     zs = []
-    for kw in ({}, {"smoother": 0, "nu": 3}, {"levels_max": 2}, {"nu": 1}):
+    for kw in ({}, {"smoother": 0, "nu": 3}, {"levels_max": 2}, {"nu": 1}, {"cf_bf16": 0},
+               {"tol_inner2": 3e-4}):
         out = gu.gpu_solve(shape, h, c, b, om, opts=mpde.mpde_default_options(**kw))
         zs.append(out["z"])
     for z in zs[1:]:
