@@ -31,6 +31,10 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 EPI_NAMES = ["store", "dot", "lanczos", "resid", "smooth", "smooth_last", "post0"]
 EPI_BYTES = [40, 40, 44, 44, 60, 52, 60]
 SCHUR_G_BYTES = 36  # x, c[7] read; g written
+# level-0 V-cycle applies (epilogues resid, smooth, smooth_last, post0) read the coefficients
+# as bf16 when mpde_options.cf_bf16 = 1: 7 coefficient values at 2 instead of 4 bytes
+BF16_EPIS = (3, 4, 5, 6)
+BF16_SAVED = 14
 
 
 def load_peaks():
@@ -260,11 +264,13 @@ def run_ours(a):
     tot_ms = sum(v[0] for v in prof.values())
     # dominant kernel: S pass 2 on level 0 (largest share of the step); level >= 1 reported too
     so_ms, so_n = prof["schur_out_l0"]
-    so_bytes = sum(p * bb for p, bb in zip(pts[9:16], EPI_BYTES))
+    bf = BF16_SAVED if opts.cf_bf16 else 0
+    so_bytes = sum(p * (bb - (bf if e in BF16_EPIS else 0))
+                   for e, (p, bb) in enumerate(zip(pts[9:16], EPI_BYTES)))
     sc_ms, sc_n = prof["schur_out"]
     sc_bytes = sum(p * bb for p, bb in zip(pts[:7], EPI_BYTES))
     sg_ms, sg_n = prof["schur_g_l0"]
-    sg_bytes = pts[7] * SCHUR_G_BYTES
+    sg_bytes = pts[7] * SCHUR_G_BYTES - bf * sum(pts[9 + e] for e in BF16_EPIS)
     peaks, peak_kind = load_peaks()
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     achieved = so_bytes / (so_ms * 1e-3) / 1e9 if so_ms > 0 else 0.0

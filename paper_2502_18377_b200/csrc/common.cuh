@@ -12,6 +12,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Programmatic dependent launch (PDL).  Inside the PCG iteration graphs every kernel ->
+// kernel edge is programmatic (mpde.cu, chunk_graph): a kernel's CTAs may be scheduled once
+// every CTA of its predecessor has started, so its launch overlaps the predecessor's tail.
+// Every kernel therefore first waits for its predecessor grid to complete and flush
+// (griddepcontrol.wait -- before ANY memory access, so read-after-write and write-after-read
+// both stay ordered), then lets its own dependents be scheduled.  Without PDL both
+// instructions are no-ops.
+#define MPDE_PDL_ENTRY() \
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
 namespace mpde {
 
 constexpr int kMaxD = 3;

@@ -14,6 +14,7 @@ constexpr int NB = 32;
 
 // symmetrise the probed columns: a = (Y + Y^T)/2, Y[j] = S_c e_j
 __global__ void k_gj_init(int n, const float* __restrict__ cols, double* __restrict__ a) {
+  MPDE_PDL_ENTRY();
   const int b = blockIdx.z;
   const int i = blockIdx.y * 32 + threadIdx.y, j = blockIdx.x * 32 + threadIdx.x;
   if (i >= n || j >= n) return;
@@ -23,6 +24,7 @@ __global__ void k_gj_init(int n, const float* __restrict__ cols, double* __restr
 }
 
 __global__ void __launch_bounds__(1024) k_gj_diag(int n, int k0, double* __restrict__ a) {
+  MPDE_PDL_ENTRY();
   __shared__ double M[NB][NB + 1];
   const int b = blockIdx.x, ty = threadIdx.y, tx = threadIdx.x;
   const int kb = min(NB, n - k0);
@@ -51,6 +53,7 @@ __global__ void __launch_bounds__(1024) k_gj_diag(int n, int k0, double* __restr
 // mode 0: row panel   A_Kj <- P A_Kj          (grid.x = column blocks)
 // mode 1: column panel A_iK <- -A_iK P        (grid.x = row blocks)
 __global__ void __launch_bounds__(1024) k_gj_panel(int n, int k0, int mode, double* __restrict__ a) {
+  MPDE_PDL_ENTRY();
   __shared__ double Pm[NB][NB + 1];
   __shared__ double T[NB][NB + 1];
   const int b = blockIdx.y, ty = threadIdx.y, tx = threadIdx.x;
@@ -83,6 +86,7 @@ __global__ void __launch_bounds__(1024) k_gj_panel(int n, int k0, int mode, doub
 
 // trailing update A_ij -= A_iK A_Kj for i, j != K (A_Kj already scaled by P)
 __global__ void __launch_bounds__(1024) k_gj_trail(int n, int k0, double* __restrict__ a) {
+  MPDE_PDL_ENTRY();
   __shared__ double L[NB][NB + 1];
   __shared__ double R[NB][NB + 1];
   const int b = blockIdx.z, ty = threadIdx.y, tx = threadIdx.x;
@@ -103,6 +107,7 @@ __global__ void __launch_bounds__(1024) k_gj_trail(int n, int k0, double* __rest
 }
 
 __global__ void k_gj_final(int n, const double* __restrict__ a, float* __restrict__ inv) {
+  MPDE_PDL_ENTRY();
   const int b = blockIdx.z;
   const int i = blockIdx.y * 32 + threadIdx.y, j = blockIdx.x * 32 + threadIdx.x;
   if (i >= n || j >= n) return;
@@ -133,6 +138,7 @@ __global__ void __launch_bounds__(256) k_coarse_gemv4(int n, const float* __rest
                                                      const float* __restrict__ r, float* e,
                                                      const float* rdot, double* part,
                                                      const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y;
   if (act && !act[v]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -212,6 +218,7 @@ __device__ __forceinline__ void restrict_axis(int I, int nf, int nc, int* f, flo
 template <int D>
 __global__ void __launch_bounds__(256) k_restrict1(Geo Gf, Geo Gc, const float* __restrict__ fine,
                                                   float* __restrict__ coarse, const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y, Pc = Gc.P, Pf = Gf.P;
   if (act && !act[v]) return;
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
@@ -281,6 +288,7 @@ __device__ __forceinline__ void prolong_axis(int i, int nf, int nc, int& I0, int
 template <int D>
 __global__ void __launch_bounds__(256) k_prolong1(Geo Gf, Geo Gc, const float* __restrict__ coarse,
                                                  float* __restrict__ fine, const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y, Pf = Gf.P, Pc = Gc.P;
   if (act && !act[v]) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -314,6 +322,7 @@ __global__ void __launch_bounds__(256) k_prolong1(Geo Gf, Geo Gc, const float* _
 template <int D>
 __global__ void __launch_bounds__(256) k_restrict1q(Geo Gf, Geo Gc, const float* __restrict__ fine,
                                                    float* __restrict__ coarse, const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y, Pc = Gc.P, Pf = Gf.P;
   if (act && !act[v]) return;
   const int I0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -376,6 +385,7 @@ __global__ void __launch_bounds__(256) k_restrict1q(Geo Gf, Geo Gc, const float*
 template <int D>
 __global__ void __launch_bounds__(256) k_prolong1q(Geo Gf, Geo Gc, const float* __restrict__ coarse,
                                                   float* __restrict__ fine, const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y, Pf = Gf.P, Pc = Gc.P;
   if (act && !act[v]) return;
   const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;

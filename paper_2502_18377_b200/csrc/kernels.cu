@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(kThreads) k_rhs_init(Geo G, const float* __res
                                                       const float* __restrict__ b,
                                                       const float* __restrict__ om,
                                                       float* __restrict__ rhs, double* part) {
+  MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(kThreads) k_residual64(Geo G, const float* __r
                                                         const double* __restrict__ z64,
                                                         float* __restrict__ r, double* part,
                                                         const int* act) {
+  MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   if (act && !act[v]) return;
@@ -213,6 +215,7 @@ template <int D>
 __global__ void __launch_bounds__(kThreads) k_apply_normal(Geo G, const float* __restrict__ c,
                                                           const float* __restrict__ z,
                                                           float* __restrict__ q) {
+  MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -253,6 +256,7 @@ template <int D, typename T>
 __global__ void __launch_bounds__(kThreads) k_ndd_solve(Geo G, const float* __restrict__ c,
                                                        const float* __restrict__ r,
                                                        float* __restrict__ t, const int* act) {
+  MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   if (act && !act[v]) return;
@@ -275,6 +279,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_rhs(Geo G, const float* __re
                                                        const float* __restrict__ r,
                                                        const float* __restrict__ t,
                                                        float* __restrict__ rt, const int* act) {
+  MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   if (act && !act[v]) return;
@@ -300,6 +305,7 @@ __global__ void __launch_bounds__(kThreads) k_backsub(Geo G, const float* __rest
                                                      const float* __restrict__ dphi,
                                                      double* __restrict__ z64, const int* act,
                                                      double* part) {
+  MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   if (act && !act[v]) return;
@@ -342,6 +348,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict(Geo Gf, Geo Gc, int nfiel
                                                       const float* __restrict__ fine,
                                                       float* __restrict__ coarse, const int* act,
                                                       int crep) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y, Pc = Gc.P, Pf = Gf.P;
   if (act && !act[v / crep]) return;
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
@@ -399,6 +406,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict(Geo Gf, Geo Gc, int nfiel
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_prolong(Geo Gf, Geo Gc, const float* __restrict__ coarse,
                                                      float* __restrict__ fine, const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y, Pf = Gf.P, Pc = Gc.P;
   if (act && !act[v]) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -459,6 +467,7 @@ __global__ void __launch_bounds__(kThreads) k_smooth_start(int P, const float* _
                                                           const float* __restrict__ coef,
                                                           int coef_stride, float* res, float* d,
                                                           float* e, const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y;
   if (act && !act[v]) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -476,6 +485,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int P, const float* __r
                                                         const float* __restrict__ p_,
                                                         const float* __restrict__ q, float* x,
                                                         float* r, double* part, const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y;
   if (act && !act[v]) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -496,6 +506,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int P, const float* __r
 __global__ void __launch_bounds__(kThreads) k_p_update(int P, const float* __restrict__ beta,
                                                       const float* __restrict__ z, float* p_,
                                                       const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y;
   if (act && !act[v]) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -508,6 +519,7 @@ __global__ void __launch_bounds__(kThreads) k_p_update(int P, const float* __res
 // y += x (W-cycle: sum of the two coarse corrections)
 __global__ void __launch_bounds__(kThreads) k_add(int P, const float* __restrict__ x, float* y,
                                                  const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y;
   if (act && !act[v]) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -520,6 +532,7 @@ __global__ void __launch_bounds__(kThreads) k_add(int P, const float* __restrict
 __global__ void __launch_bounds__(kThreads) k_scale(int P, const float* __restrict__ s,
                                                    const float* __restrict__ x, float* y,
                                                    const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y;
   if (act && !act[v]) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -536,6 +549,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_update(int P, const float* __re
                                                        const float* __restrict__ alpha,
                                                        const float* __restrict__ beta,
                                                        double* part) {
+  MPDE_PDL_ENTRY();
   const int b = blockIdx.y;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   double dot = 0.0;
@@ -551,6 +565,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_update(int P, const float* __re
 
 // deterministic pseudo-random start vector (counter-based hash), values in [-1, 1)
 __global__ void __launch_bounds__(kThreads) k_rand_fill(int P, float* y, uint32_t seed) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
@@ -565,6 +580,7 @@ __global__ void __launch_bounds__(kThreads) k_rand_fill(int P, float* y, uint32_
 
 // identity probes: x[(b*Pc + j)][p] = (p == j)
 __global__ void __launch_bounds__(kThreads) k_identity(int Pc, float* x) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= Pc) return;
@@ -594,6 +610,7 @@ __device__ __forceinline__ void pcg_fail(const PdeState& st, int v, double val) 
 // shuffle tree -- deterministic), lane 0 runs the per-PDE logic.
 __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt, float tol2,
                          int max_iters) {
+  MPDE_PDL_ENTRY();
   const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (v >= B) return;
   double S_ = 0.0;
@@ -771,6 +788,7 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
 
 // count of PDEs still active (polled by the host)
 __global__ void k_count_active(int B, const int* act, int* out) {
+  MPDE_PDL_ENTRY();
   __shared__ int s;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
@@ -784,6 +802,7 @@ __global__ void k_count_active(int B, const int* act, int* out) {
 // Saad "Iterative Methods" Alg. 12.1 recurrence): d_k = alpha_k d_{k-1} + beta_k D^-1 res_k
 __global__ void k_smooth_coef(int B, int nu, int kind, float theta, float ratio,
                               const double* lmax, float* coef) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= B) return;
   const double lm = lmax[v] > 0 ? lmax[v] : 1.0;
@@ -825,6 +844,7 @@ __global__ void __launch_bounds__(kThreads) k_grad(Geo G, const float* __restric
                                                   const double* __restrict__ dz64,
                                                   float* __restrict__ gc, float* __restrict__ gb,
                                                   float* __restrict__ gw, float* __restrict__ dz_out) {
+  MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -860,6 +880,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_out(Geo G, const float* __rest
                                                      const double* __restrict__ z64,
                                                      float* __restrict__ z,
                                                      float* __restrict__ rho) {
+  MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -878,6 +899,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_out(Geo G, const float* __rest
 // out[j] = sum_b x[b][j], fixed summation order (deterministic)
 __global__ void __launch_bounds__(kThreads) k_batch_sum(const float* __restrict__ x, int B,
                                                        int64_t n, float* __restrict__ out) {
+  MPDE_PDL_ENTRY();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   double acc = 0.0;
@@ -887,16 +909,19 @@ __global__ void __launch_bounds__(kThreads) k_batch_sum(const float* __restrict_
 
 __global__ void __launch_bounds__(kThreads) k_f2bf(size_t n, const float* __restrict__ a,
                                                    __nv_bfloat16* __restrict__ b) {
+  MPDE_PDL_ENTRY();
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = __float2bfloat16_rn(a[i]);
 }
 
 __global__ void __launch_bounds__(kThreads) k_d2f(size_t n, const double* __restrict__ a, float* __restrict__ b) {
+  MPDE_PDL_ENTRY();
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = float(a[i]);
 }
 
 __global__ void k_stats_out(int B, PdeState st, mpde_stats* out) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= B) return;
   out[v].iters = st.iters[v];

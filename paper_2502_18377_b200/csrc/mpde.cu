@@ -439,6 +439,7 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
 }
 
 __global__ void k_fill_int(int n, int* a, int v) {
+  MPDE_PDL_ENTRY();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
 }
@@ -587,6 +588,42 @@ std::mutex g_graph_mu;
 std::map<std::string, std::pair<cudaGraphExec_t, unsigned long long>> g_graphs;
 cudaStream_t g_capture_stream = nullptr;
 
+// Programmatic dependent launch inside the PCG graphs (env MPDE_PDL, default 1): every
+// kernel -> kernel edge of the captured chain becomes a programmatic edge, so the next
+// kernel's CTAs are scheduled while the previous kernel drains; every kernel starts with
+// MPDE_PDL_ENTRY() (griddepcontrol.wait before any memory access), which keeps the order.
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPDE_PDL");
+    on = e ? atoi(e) : 1;
+  }
+  return on != 0;
+}
+
+static int make_edges_programmatic(cudaGraph_t graph) {
+  size_t ne = 0;
+  CK(cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &ne));
+  if (ne == 0) return MPDE_OK;
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  std::vector<cudaGraphEdgeData> ed(ne);
+  CK(cudaGraphGetEdges_v2(graph, from.data(), to.data(), ed.data(), &ne));
+  for (size_t i = 0; i < ne; ++i) {
+    cudaGraphNodeType ta, tb;
+    CK(cudaGraphNodeGetType(from[i], &ta));
+    CK(cudaGraphNodeGetType(to[i], &tb));
+    if (ta != cudaGraphNodeTypeKernel || tb != cudaGraphNodeTypeKernel) continue;
+    if (ed[i].type == cudaGraphDependencyTypeProgrammatic) continue;
+    CK(cudaGraphRemoveDependencies_v2(graph, &from[i], &to[i], &ed[i], 1));
+    cudaGraphEdgeData pe{};
+    pe.from_port = cudaGraphKernelNodePortProgrammatic;
+    pe.to_port = 0;
+    pe.type = cudaGraphDependencyTypeProgrammatic;
+    CK(cudaGraphAddDependencies_v2(graph, &from[i], &to[i], &pe, 1));
+  }
+  return MPDE_OK;
+}
+
 template <class F>
 int chunk_graph(mpde_hierarchy* h, int k, F& iteration, cudaGraphExec_t* out,
                 unsigned long long* nodes) {
@@ -624,6 +661,11 @@ int chunk_graph(mpde_hierarchy* h, int k, F& iteration, cudaGraphExec_t* out,
       n += ty == cudaGraphNodeTypeKernel;
     }
   }
+  if (pdl_enabled())
+    if (int rc2 = make_edges_programmatic(graph)) {
+      cudaGraphDestroy(graph);
+      return rc2;
+    }
   cudaGraphExec_t exec = nullptr;
   const cudaError_t e2 = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -637,6 +679,7 @@ int chunk_graph(mpde_hierarchy* h, int k, F& iteration, cudaGraphExec_t* out,
 
 // k_dot partial for rr0: reuse pcg_update with alpha = 0 would touch p; use a dedicated path
 __global__ void k_dot_self(int P, const float* __restrict__ r, double* part, const int* act) {
+  MPDE_PDL_ENTRY();
   const int v = blockIdx.y;
   if (act && !act[v]) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;

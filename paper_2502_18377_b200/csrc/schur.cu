@@ -26,6 +26,7 @@ namespace mpde {
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_schur_coef(Geo G, const float* __restrict__ c,
                                                         float* __restrict__ cf) {
+  MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D, NC = 2 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_h(Geo G, const float* __rest
                                                      const float* __restrict__ x,
                                                      T* __restrict__ hout, const int* act,
                                                      unsigned long long* pts) {
+  MPDE_PDL_ENTRY();
   constexpr int NC = 2 + 2 * D;
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_s(Geo G, const float* __rest
                                                      const float* __restrict__ x,
                                                      const T* __restrict__ hb, EpiArgs A,
                                                      const int* act) {
+  MPDE_PDL_ENTRY();
   constexpr int NC = 2 + 2 * D;
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
@@ -206,6 +209,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_s(Geo G, const float* __rest
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_schur_diag(Geo G, const float* __restrict__ cf,
                                                         float* __restrict__ dinv) {
+  MPDE_PDL_ENTRY();
   constexpr int NC = 2 + 2 * D;
   const int v = blockIdx.y, P = G.P;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -556,6 +560,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_h_v4(Geo G, const CF* __rest
                                                         const float* __restrict__ x,
                                                         T* __restrict__ hout, const int* act,
                                                         unsigned long long* pts, int remap) {
+  MPDE_PDL_ENTRY();
   constexpr int NC = 2 + 2 * D;
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
@@ -581,6 +586,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_s_v4(Geo G, const CF* __rest
                                                         const float* __restrict__ x,
                                                         const T* __restrict__ hb, EpiArgs A,
                                                         const int* act, int remap) {
+  MPDE_PDL_ENTRY();
   constexpr int NC = 2 + 2 * D;
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
@@ -960,6 +966,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_schur_s_b22(Geo G, const CF* __
                                                          const float* __restrict__ x,
                                                          const float* __restrict__ hb, EpiArgs A,
                                                          const int* act, int remap) {
+  MPDE_PDL_ENTRY();
   // BX = 1: 2x2 blocking in (t, x); BX = 0: 2x1 blocking in t only (fewer registers)
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
@@ -1079,6 +1086,7 @@ static inline size_t fused_smem_floats(int n2) {
 template <int EPI>
 __global__ void k_schur_fused(Geo G, const float* __restrict__ cf, int crep,
                               const float* __restrict__ x, EpiArgs A, const int* act) {
+  MPDE_PDL_ENTRY();
   extern __shared__ __align__(16) float fsm[];
   const int v = blockIdx.y, P = G.P, pde = v / crep;
   if (act && !act[pde]) return;
@@ -1407,6 +1415,7 @@ __global__ void __launch_bounds__(4 * NY) k_schur_s_tile(Geo G, const float* __r
                                                         const float* __restrict__ x,
                                                         const float* __restrict__ hb, EpiArgs A,
                                                         const int* act) {
+  MPDE_PDL_ENTRY();
   constexpr int NQ = NY / 4, NTH = 4 * NY;  // threads = kTT * kTX * NQ
   extern __shared__ __align__(16) float tsm[];
   const int v = blockIdx.y, P = G.P, pde = v / crep;
@@ -1636,6 +1645,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_hy(Geo G, const float* __res
                                                       const float* __restrict__ x,
                                                       float* __restrict__ gout, const int* act,
                                                       unsigned long long* pts) {
+  MPDE_PDL_ENTRY();
   __shared__ __align__(16) float sx[4 * kThreads], sw1[4 * kThreads], sw2[4 * kThreads],
       sh[4 * kThreads];
   const int v = blockIdx.y, P = G.P, pde = v / crep;

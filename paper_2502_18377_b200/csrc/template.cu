@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(kThreads) k_template_coeff(TmplArgs t, const f
                                                              const float* __restrict__ feat,
                                                              float* __restrict__ coeff,
                                                              float* __restrict__ rhs) {
+  MPDE_PDL_ENTRY();
   __shared__ float th[kTmplMaxR * kTmplMaxK];
   for (int i = threadIdx.x; i < t.R * K; i += blockDim.x) th[i] = theta[i];
   __syncthreads();
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(kThreads) k_template_grad(TmplArgs t, const fl
                                                             const float* __restrict__ gb,
                                                             float* __restrict__ gfeat,
                                                             double* __restrict__ part) {
+  MPDE_PDL_ENTRY();
   __shared__ float th[kTmplMaxR * kTmplMaxK];
   __shared__ double acc[kThreads / 32][kTmplMaxR * kTmplMaxK];
   const int NP = t.R * K;
@@ -145,6 +147,7 @@ __global__ void __launch_bounds__(kThreads) k_template_grad(TmplArgs t, const fl
 // grad_theta[j] = sum over nparts partials (one CTA per j, fixed-order tree)
 __global__ void __launch_bounds__(kThreads) k_template_reduce(const double* __restrict__ part, int nparts,
                                                               int NP, float* __restrict__ gtheta) {
+  MPDE_PDL_ENTRY();
   __shared__ double s[kThreads];
   const int j = blockIdx.x;
   double a = 0.0;
