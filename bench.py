@@ -357,6 +357,85 @@ def run_ours(a):
                              "build -> fwd -> bwd -> dl/dtheta -> all-reduce of [8][3] fp32",
                  "allreduce_bytes": gth.numel() * 4}
 
+    # ---- §8(f) N1: the same C4 step with FGMRES(20) instead of PCG (the paper's Krylov method)
+    fstep = None
+    if not a.no_fgmres:
+        fopts = mpde.mpde_default_options(krylov=1, restart=20)
+        fws = torch.empty(mpde.mpde_workspace_bytes(prob, fopts), dtype=torch.uint8, device=dev)
+
+        def fstep_fn(i):
+            s = sets[i % 2]
+            h = mpde.mpde_build_hierarchy(prob, fopts, s["c"], fws, stream)
+            mpde.mpde_solve_fwd(h, s["b"], s["om"], z, stats_f, stream)
+            mpde.mpde_solve_bwd(h, s["b"], z, s["g"], gc, gb, gw, None, stats_b, stream)
+            mpde.mpde_batch_sum(gc, gsum, stream)
+            allreduce_coeff_grad(gsum)
+            mpde.mpde_destroy_hierarchy(h)
+
+        for i in range(a.warmup):
+            fstep_fn(i)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0e, f1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0e.record(stream)
+        for i in range(a.steps):
+            fstep_fn(i)
+        f1e.record(stream)
+        torch.cuda.synchronize()
+        fms = max_over_ranks(f0e.elapsed_time(f1e), device=dev)
+        ff, fb = stats_of(stats_f), stats_of(stats_b)
+        fstep = {"value": world * B * a.steps / (fms / 1e3), "unit": "PDE solves/s (fwd+bwd)",
+                 "ms_per_step": fms / a.steps,
+                 "workload": "C4 step (build -> fwd -> bwd -> grad_c all-reduce) with FGMRES(20) "
+                             "+ the same V-cycle (krylov=1) instead of PCG",
+                 "fwd_iters_mean": sum(x[0] for x in ff) / len(ff),
+                 "bwd_iters_mean": sum(x[0] for x in fb) / len(fb),
+                 "not_converged": sum(1 for x in ff + fb if x[2] != 0)}
+        del fws
+
+    # ---- §8(f) N3: the dense path (levels_max = 1: exact S^-1) on C1-sized 1D problems ----
+    dstep = None
+    if not a.no_dense:
+        c1 = synth.CONFIGS["C1"]
+        DB = 2048
+        d1 = synth.make_batch("C1")
+        g1 = synth.make_g("C1")
+        rep = lambda x: torch.from_numpy(np.repeat(x, DB, axis=0)).to(dev)
+        dc, db_, dom, dg = rep(d1["c"]), rep(d1["b"]), rep(d1["omega"]), rep(g1)
+        dprob = mpde.make_problem(c1.shape, c1.h, DB)
+        dopts = mpde.mpde_default_options(levels_max=1)
+        dws = torch.empty(mpde.mpde_workspace_bytes(dprob, dopts), dtype=torch.uint8, device=dev)
+        dz, dgc = torch.empty_like(dc), torch.empty_like(dc)
+        dgb, dgw = torch.empty_like(db_), torch.empty_like(db_)
+        dsf = torch.zeros((DB, 5), dtype=torch.int32, device=dev)
+        dsb = torch.zeros((DB, 5), dtype=torch.int32, device=dev)
+
+        def dstep_fn():
+            h = mpde.mpde_build_hierarchy(dprob, dopts, dc, dws, stream)
+            mpde.mpde_solve_fwd(h, db_, dom, dz, dsf, stream)
+            mpde.mpde_solve_bwd(h, db_, dz, dg, dgc, dgb, dgw, None, dsb, stream)
+            mpde.mpde_destroy_hierarchy(h)
+
+        for i in range(a.warmup):
+            dstep_fn()
+        torch.cuda.synchronize()
+        d0e, d1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0e.record(stream)
+        for i in range(a.steps):
+            dstep_fn()
+        d1e.record(stream)
+        torch.cuda.synchronize()
+        dms = max_over_ranks(d0e.elapsed_time(d1e), device=dev)
+        dst = dsf.cpu()
+        dstep = {"value": world * DB * a.steps / (dms / 1e3), "unit": "PDE solves/s (fwd+bwd)",
+                 "ms_per_step": dms / a.steps,
+                 "workload": f"C1 heat 16x16 replicated to batch {DB} per GPU, dense path "
+                             "(levels_max=1: probed S, fp64 Gauss-Jordan inverse, GEMV PCG)",
+                 "fwd_iters_max": int(dst[:, 0].max()),
+                 "ws_bytes": int(dws.numel())}
+        del dws
+
     if rank == 0:
         cpu = None
         if world == 1 and not a.no_cpu:
@@ -392,6 +471,8 @@ def run_ours(a):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "template_step": tstep,
+            "fgmres_step": fstep,
+            "dense_step": dstep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -436,6 +517,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-template", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-fgmres", action="store_true")
     a = ap.parse_args()
     if a.impl == "reference":
         run_reference(a)

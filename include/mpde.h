@@ -108,6 +108,13 @@ typedef struct {
                          of S as bf16 (half the bytes); S~ stays symmetric PSD, so the
                          preconditioner is still a fixed SPD map.  The PCG operator, the
                          refinement residual and the gradients keep fp32 / fp64 (default 1) */
+  int32_t krylov;     /* inner Krylov method on the condensed system: 0 = PCG (default; needs
+                         the fixed SPD V-cycle), 1 = FGMRES(restart) with the same V-cycle as a
+                         flexible right preconditioner -- the paper's method (SURVEY
+                         §8(f) N1); its |g_{j+1}| is the true residual ||rt - S x||, so the same
+                         tol_inner / tol_inner2 / max_iters apply                           */
+  int32_t restart;    /* FGMRES restart length m, 1..32 (default 20; workspace grows by
+                         (2m+1) scalar fields per PDE)                                      */
 } mpde_options;
 
 /* one per PDE, device memory, written by mpde_solve_fwd / mpde_solve_bwd */

@@ -76,6 +76,29 @@ struct PdeState {
   float tol2_later;  // (PCG relative tolerance of refinement passes >= 2)^2
 };
 
+// FGMRES(m) (fgmres.cu, opts.krylov = 1): per-PDE Arnoldi state, arrays over the batch
+enum { GM_BEGIN = 0, GM_RESTART = 1, GM_DOTS0 = 2, GM_DOTS1 = 3, GM_NORM = 4, GM_SOLVE = 5 };
+struct GmState {
+  double* H;     // [B][m+1][m] Hessenberg (rotated in place: upper triangle R)
+  double* g;     // [B][m+1] rotated residual vector
+  double* cs;    // [B][m] Givens cosines
+  double* sn;    // [B][m] Givens sines
+  double* coef;  // [B][m+1] Gram-Schmidt coefficients of the current step / y at cycle end
+  int* k;        // [B] Arnoldi steps of the current cycle
+  int* gact;     // [B] PDE iterating at the start of the current cycle
+  float* scl;    // [B] 1 / norm of the newest basis vector
+};
+int gm_tiles(int P);
+void launch_gm_mdot(int P, int B, int j1, int m, const float* V, const float* w, double* part,
+                    const int* act, cudaStream_t s);
+void launch_gm_update(int P, int B, int j1, int m, const float* V, const double* coef, float* w,
+                      double* part, const int* act, cudaStream_t s);
+void launch_gm_scale(int P, int B, const float* sc, float* y, const int* act, cudaStream_t s);
+void launch_gm_resid(int P, int B, int m, const float* rt, float* y, int first, double* part,
+                     const int* act, cudaStream_t s);
+void launch_gm_xupdate(int P, int B, int m, const float* Z, const GmState& g, float* x,
+                       cudaStream_t s);
+
 int ntiles(int P);
 extern std::atomic<unsigned long long> g_launch_count;  // host-side count of kernel launches
 int coarse_gemv_blocks(int n);
@@ -147,6 +170,8 @@ void launch_coarse_gemv(int n, int nvec, const float* sinv, const float* r, floa
                         const float* rdot, double* part, const int* act, cudaStream_t s);
 void launch_scalar(int op, int B, const PdeState& st, const double* part, int nt, float tol2,
                    int max_iters, cudaStream_t s);
+void launch_gm_scalar(int op, int j, int m, int P, int B, const PdeState& st, const GmState& g,
+                      const double* part, float tol2, int max_iters, cudaStream_t s);
 void launch_count_active(int B, const int* act, int* out, cudaStream_t s);
 void launch_smooth_coef(int B, int nu, int kind, float theta, float ratio, const double* lmax,
                         float* coef, cudaStream_t s);

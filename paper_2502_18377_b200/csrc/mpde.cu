@@ -83,6 +83,10 @@ int validate(const mpde_problem* pr, const mpde_options* op) {
     return set_err(MPDE_ERR_UNSUPPORTED, "smoother must be 0 (Jacobi) or 1 (Chebyshev)");
   if (op->cf_bf16 != 0 && op->cf_bf16 != 1)
     return set_err(MPDE_ERR_INVALID_ARG, "cf_bf16 must be 0 or 1");
+  if (op->krylov != 0 && op->krylov != 1)
+    return set_err(MPDE_ERR_UNSUPPORTED, "krylov must be 0 (PCG) or 1 (FGMRES)");
+  if (op->krylov == 1 && (op->restart < 1 || op->restart > 32))
+    return set_err(MPDE_ERR_INVALID_ARG, "restart must be in 1..32 (got %d)", op->restart);
   if (op->nu < 1 || op->nu > 16) return set_err(MPDE_ERR_INVALID_ARG, "nu must be in 1..16");
   if (op->max_refine < 1 || op->max_iters < 1 || op->poll_every < 1)
     return set_err(MPDE_ERR_INVALID_ARG, "max_refine, max_iters, poll_every must be >= 1");
@@ -338,6 +342,10 @@ struct mpde_hierarchy {
   int* ones;     // [B] all 1
   float* rho;    // [B][P] equation residual b - c.z* of the last forward (fp64-derived)
   const float* rho_b;  // rhs_b it was computed for
+  // FGMRES (opts.krylov = 1): basis V [m+1][B][P], preconditioned basis Z [m][B][P]
+  float *gmV = nullptr, *gmZ = nullptr;
+  double* gmpart = nullptr;  // [B][m+1][gm_tiles(P)]
+  GmState gm{};
 };
 
 inline bool f64_outer(const mpde_hierarchy* h) { return h->opts.precision >= 1; }
@@ -418,6 +426,20 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
   h->st.errest = bp.take<double>(B);
   h->d_count = bp.take<int>(2);
   h->ones = bp.take<int>(B);
+  if (op->krylov == 1) {
+    const int m = op->restart;
+    h->gmV = bp.take<float>((size_t)(m + 1) * B * P);
+    h->gmZ = bp.take<float>((size_t)m * B * P);
+    h->gmpart = bp.take<double>((size_t)B * (m + 1) * gm_tiles(P));
+    h->gm.H = bp.take<double>((size_t)B * (m + 1) * m);
+    h->gm.g = bp.take<double>((size_t)B * (m + 1));
+    h->gm.cs = bp.take<double>((size_t)B * m);
+    h->gm.sn = bp.take<double>((size_t)B * m);
+    h->gm.coef = bp.take<double>((size_t)B * (m + 1));
+    h->gm.k = bp.take<int>(B);
+    h->gm.gact = bp.take<int>(B);
+    h->gm.scl = bp.take<float>(B);
+  }
   // union: full-system solve vectors | coarsest probing scratch
   const size_t u0 = bp.off;
   h->rfull = bp.take<float>((size_t)B * M * P);
@@ -755,6 +777,85 @@ int pcg(mpde_hierarchy* h, cudaStream_t s) {
   return MPDE_OK;
 }
 
+// FGMRES(m) on the condensed system S x = rp (level 0), x0 = 0, with the V-cycle as a flexible
+// right preconditioner (fgmres.cu).  One restart cycle (m Arnoldi steps + update +
+// restart residual) is one CUDA graph; the host polls the active count between cycles.
+int fgmres(mpde_hierarchy* h, cudaStream_t s) {
+  const int B = h->B, P = h->P, m = h->opts.restart;
+  const size_t BP = (size_t)B * P;
+  const float tol2 = h->opts.tol_inner * h->opts.tol_inner;
+  int* act = h->st.act;
+  Level& l0 = h->lv[0];
+  float* V = h->gmV;
+  float* Z = h->gmZ;
+  double* gp = h->gmpart;
+  const GmState& g = h->gm;
+  const int mi = h->opts.max_iters;
+  CK(cudaMemsetAsync(h->x, 0, sizeof(float) * BP, s));
+  ++g_launch_count;
+  PROF(6, s, launch_gm_resid(P, B, m, h->rp, V, 1, gp, act, s));
+  PROF(7, s, launch_gm_scalar(GM_BEGIN, 0, m, P, B, h->st, g, gp, tol2, mi, s));
+  PROF(6, s, launch_gm_scale(P, B, g.scl, V, act, s));
+  CKL();
+  float* e_saved = l0.e;
+  auto cycle = [&](cudaStream_t st) -> int {
+    for (int j = 0; j < m; ++j) {
+      float* Vj = V + j * BP;
+      float* Zj = Z + j * BP;
+      float* w = V + (j + 1) * BP;
+      l0.e = Zj;  // the V-cycle accumulates its correction straight into Z_j
+      const int rc = vcycle(h, 0, Vj, nullptr, h->part, act, st);
+      l0.e = e_saved;
+      if (rc) return rc;
+      EpiArgs A;
+      A.y = w;
+      if (int rc2 = schur_apply(h, 0, EPI_STORE, B, 1, Zj, A, act, f64_pcg(h), st)) return rc2;
+      for (int pass = 0; pass < 2; ++pass) {  // CGS2
+        PROF(6, st, launch_gm_mdot(P, B, j + 1, m, V, w, gp, act, st));
+        PROF(7, st, launch_gm_scalar(pass ? GM_DOTS1 : GM_DOTS0, j, m, P, B, h->st, g, gp, tol2, mi, st));
+        PROF(6, st, launch_gm_update(P, B, j + 1, m, V, g.coef, w, gp, act, st));
+      }
+      PROF(7, st, launch_gm_scalar(GM_NORM, j, m, P, B, h->st, g, gp, tol2, mi, st));
+      PROF(6, st, launch_gm_scale(P, B, g.scl, w, act, st));
+      CKL();
+    }
+    PROF(7, st, launch_gm_scalar(GM_SOLVE, 0, m, P, B, h->st, g, nullptr, tol2, mi, st));
+    PROF(6, st, launch_gm_xupdate(P, B, m, Z, g, h->x, st));
+    // restart: V_0 = (rp - S x) / ||rp - S x|| for the PDEs still iterating
+    EpiArgs A;
+    A.y = V;
+    if (int rc = schur_apply(h, 0, EPI_STORE, B, 1, h->x, A, act, f64_pcg(h), st)) return rc;
+    PROF(6, st, launch_gm_resid(P, B, m, h->rp, V, 0, gp, act, st));
+    PROF(7, st, launch_gm_scalar(GM_RESTART, 0, m, P, B, h->st, g, gp, tol2, mi, st));
+    PROF(6, st, launch_gm_scale(P, B, g.scl, V, act, st));
+    CKL();
+    return MPDE_OK;
+  };
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long nodes = 0;
+  if (!g_prof.on && h->opts.use_graphs) {
+    if (int rc = chunk_graph(h, 1, cycle, &exec, &nodes)) return rc;
+  }
+  const int ncycles = (mi + m - 1) / m + 1;
+  for (int j = 0; j < ncycles; ++j) {
+    if (exec) {
+      CK(cudaGraphLaunch(exec, s));
+      g_launch_count += nodes;
+    } else if (int rc = cycle(s)) {
+      return rc;
+    }
+    PROF(7, s, launch_count_active(B, h->st.act, h->d_count + (j & 1), s));
+    CK(cudaMemcpyAsync(h->h_count + (j & 1), h->d_count + (j & 1), sizeof(int),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(h->ev[j & 1], s));
+    if (j >= 1) {
+      CK(cudaEventSynchronize(h->ev[(j - 1) & 1]));
+      if (h->h_count[(j - 1) & 1] == 0) break;
+    }
+  }
+  return MPDE_OK;
+}
+
 // Solve N z = rhs for every PDE (refinement loop); result in h->z64.  rhs == nullptr:
 // rhs = A^T d from (b, om), formed in fp64 inside the residual kernel.
 int solve_core(mpde_hierarchy* h, const float* rhs, const float* b, const float* om,
@@ -774,7 +875,7 @@ int solve_core(mpde_hierarchy* h, const float* rhs, const float* b, const float*
     PROF(3, s, launch_ndd_solve(l0.G, B, l0.c, h->rfull, h->tfull, h->st.act, f64_outer(h), s));
     PROF(3, s, launch_schur_rhs(l0.G, B, l0.c, h->rfull, h->tfull, h->rp, h->st.act, f64_outer(h), s));
     CKL();
-    if (int rc = pcg(h, s)) return rc;
+    if (int rc = h->opts.krylov == 1 ? fgmres(h, s) : pcg(h, s)) return rc;
     // re-activate every PDE still being refined (PCG deactivated converged ones)
     PROF(7, s, launch_scalar(SC_REACT, B, h->st, h->part, nt, 0.f, 0, s));
     PROF(4, s, launch_backsub(l0.G, B, l0.c, h->rfull, h->x, h->z64, h->st.act, f64_outer(h),
@@ -812,6 +913,8 @@ mpde_options mpde_default_options(void) {
   o.precision = 1;
   o.use_graphs = 1;
   o.cf_bf16 = 1;
+  o.krylov = 0;
+  o.restart = 20;
   o.tol_inner2 = 3e-3f;  // tools/calib_tol.py: -16% iterations on C4, e_z <= 2.7e-5 on C2-C4
   return o;
 }

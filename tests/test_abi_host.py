@@ -89,3 +89,20 @@ def test_template_terms_and_validation(mp):
     # fp64 partials of grad_theta: one per (PDE, CTA of 1024 points) and (|M|+1) K entries
     assert mp.mpde_template_workspace_bytes(pr, mp.make_template(2, 1)) == 8 * 32 * 128 * 8 * 3
     assert mp.lib().mpde_template_workspace_bytes(C.byref(pr), C.byref(mp.make_template(2, 7))) == 0
+
+
+def test_fgmres_options_and_workspace(mp):
+    """krylov = 1 (FGMRES(m), §8(f) N1): default off, restart 20; the workspace grows by
+    (2m+1) scalar fields per PDE plus the per-PDE Arnoldi state; restart outside 1..32 and an
+    unknown Krylov method are rejected (workspace 0)."""
+    import ctypes as C
+    o = mp.mpde_default_options()
+    assert o.krylov == 0 and o.restart == 20
+    pr = mp.make_problem((32, 64, 64), (0.01, 1 / 64, 1 / 64), 4)
+    w0 = mp.mpde_workspace_bytes(pr, o)
+    for m in (1, 20, 32):
+        w = mp.mpde_workspace_bytes(pr, mp.mpde_default_options(krylov=1, restart=m))
+        assert w - w0 >= (2 * m + 1) * 4 * 32 * 64 * 64 * 4
+    lib = mp.lib()
+    for kw in ({"krylov": 1, "restart": 0}, {"krylov": 1, "restart": 33}, {"krylov": 2}):
+        assert lib.mpde_workspace_bytes(C.byref(pr), C.byref(mp.mpde_default_options(**kw))) == 0
