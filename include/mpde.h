@@ -113,7 +113,7 @@ typedef struct {
                          flexible right preconditioner -- the paper's method (SURVEY
                          §8(f) N1); its |g_{j+1}| is the true residual ||rt - S x||, so the same
                          tol_inner / tol_inner2 / max_iters apply                           */
-  int32_t restart;    /* FGMRES restart length m, 1..32 (default 20; workspace grows by
+  int32_t restart;    /* FGMRES restart length m, 1..32 (default 30; workspace grows by
                          (2m+1) scalar fields per PDE)                                      */
 } mpde_options;
 

@@ -235,7 +235,7 @@ def _equilibration(N):
 
 
 def solve_normal(A, rhs, method: str = "auto", tol: float = 1e-12, maxiter: int = 200000,
-                 info: dict | None = None):
+                 info: dict | None = None, strict: bool = True):
     """Solve A^T A x = rhs (Eq. 9).
 
     method: 'dense' (SVD), 'lu' (SuperLU on S A^T A S + 2 fp64 refinement steps with
@@ -290,6 +290,9 @@ def solve_normal(A, rhs, method: str = "auto", tol: float = 1e-12, maxiter: int 
             rz = rz_new
         info["iters"] = it
         info["rel_res"] = float(np.linalg.norm(rhs - N @ x) / nrm)
+        if strict and not (info["rel_res"] <= 1e-6):
+            raise RuntimeError(f"oracle CG did not converge: rel_res {info['rel_res']:.3e} after "
+                               f"{it} iterations (ill-conditioned system; use method='lu')")
         return x
     raise ValueError(method)
 

@@ -24,23 +24,45 @@ int gm_tiles(int P) { return (P + kGmTile - 1) / kGmTile; }
 // P % 4 == 0 is not required: the vector kernels handle the tail point by point.
 __device__ __forceinline__ double gm_block_sum(double v) { return block_sum(v); }
 
-// part[(v * (m+1) + i) * nt + tile] = <w_v, V_i,v> over the tile, i < j1
+// part[(v * (m+1) + i) * nt + tile] = <w_v, V_i,v> over the tile, i < j1.  Each thread keeps
+// its kGmTile / kThreads points of w in registers; every V_i is read once (coalesced), its
+// per-thread partial reduced by warp shuffles into smem [warp][i]; one barrier at the end.
 __global__ void __launch_bounds__(kThreads) k_gm_mdot(int P, int j1, int m1, const float* V,
                                                       size_t BP, const float* w, double* part,
                                                       const int* act) {
   MPDE_PDL_ENTRY();
+  constexpr int kPer = kGmTile / kThreads;
+  __shared__ double red[kThreads / 32][33];
   const int v = blockIdx.y;
   if (act && !act[v]) return;
   const int nt = gridDim.x;
-  const int p0 = blockIdx.x * kGmTile;
-  const int p1 = min(P, p0 + kGmTile);
+  const int p0 = blockIdx.x * kGmTile + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* wv = w + (size_t)v * P;
+  float wr[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int p = p0 + k * kThreads;
+    wr[k] = p < P ? wv[p] : 0.f;
+  }
   for (int i = 0; i < j1; ++i) {
     const float* Vi = V + i * BP + (size_t)v * P;
     double d = 0.0;
-    for (int p = p0 + threadIdx.x; p < p1; p += kThreads) d += double(wv[p]) * double(Vi[p]);
-    d = gm_block_sum(d);
-    if (threadIdx.x == 0) part[((size_t)v * m1 + i) * nt + blockIdx.x] = d;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int p = p0 + k * kThreads;
+      if (p < P) d += double(wr[k]) * double(Vi[p]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if (lane == 0) red[warp][i] = d;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < j1; i += kThreads) {
+    double d = 0.0;
+#pragma unroll
+    for (int k = 0; k < kThreads / 32; ++k) d += red[k][i];
+    part[((size_t)v * m1 + i) * nt + blockIdx.x] = d;
   }
 }
 

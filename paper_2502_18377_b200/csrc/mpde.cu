@@ -777,6 +777,16 @@ int pcg(mpde_hierarchy* h, cudaStream_t s) {
   return MPDE_OK;
 }
 
+// Gram-Schmidt passes per Arnoldi step (env MPDE_GM_REORTH, default 1 = CGS2)
+static int gm_passes() {
+  static int n = -1;
+  if (n < 0) {
+    const char* e = getenv("MPDE_GM_REORTH");
+    n = (e && atoi(e) == 0) ? 1 : 2;
+  }
+  return n;
+}
+
 // FGMRES(m) on the condensed system S x = rp (level 0), x0 = 0, with the V-cycle as a flexible
 // right preconditioner (fgmres.cu).  One restart cycle (m Arnoldi steps + update +
 // restart residual) is one CUDA graph; the host polls the active count between cycles.
@@ -810,7 +820,7 @@ int fgmres(mpde_hierarchy* h, cudaStream_t s) {
       EpiArgs A;
       A.y = w;
       if (int rc2 = schur_apply(h, 0, EPI_STORE, B, 1, Zj, A, act, f64_pcg(h), st)) return rc2;
-      for (int pass = 0; pass < 2; ++pass) {  // CGS2
+      for (int pass = 0; pass < gm_passes(); ++pass) {  // CGS2 (MPDE_GM_REORTH=0: one CGS pass)
         PROF(6, st, launch_gm_mdot(P, B, j + 1, m, V, w, gp, act, st));
         PROF(7, st, launch_gm_scalar(pass ? GM_DOTS1 : GM_DOTS0, j, m, P, B, h->st, g, gp, tol2, mi, st));
         PROF(6, st, launch_gm_update(P, B, j + 1, m, V, g.coef, w, gp, act, st));
@@ -914,7 +924,7 @@ mpde_options mpde_default_options(void) {
   o.use_graphs = 1;
   o.cf_bf16 = 1;
   o.krylov = 0;
-  o.restart = 20;
+  o.restart = 30;
   o.tol_inner2 = 3e-3f;  // tools/calib_tol.py: -16% iterations on C4, e_z <= 2.7e-5 on C2-C4
   return o;
 }

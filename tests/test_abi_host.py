@@ -97,7 +97,7 @@ def test_fgmres_options_and_workspace(mp):
     unknown Krylov method are rejected (workspace 0)."""
     import ctypes as C
     o = mp.mpde_default_options()
-    assert o.krylov == 0 and o.restart == 20
+    assert o.krylov == 0 and o.restart == 30
     pr = mp.make_problem((32, 64, 64), (0.01, 1 / 64, 1 / 64), 4)
     w0 = mp.mpde_workspace_bytes(pr, o)
     for m in (1, 20, 32):

@@ -348,3 +348,22 @@ def test_synth_deterministic_float32():
     assert np.array_equal(a["c"], b["c"]) and np.array_equal(a["omega"], b["omega"])
     assert not np.array_equal(a["c"][0], a["c"][1])
     assert field_index(2, 2) == 6
+
+
+def test_oracle_cg_refuses_unconverged():
+    """The oracle never returns an unconverged CG answer as ground truth: a capped run
+    raises (strict), and returns only when the caller asks for a timing sample."""
+    import pytest
+    from oracle.neurlp import solve_normal
+    pr = Problem((8, 9), (0.1, 0.1))
+    rng = np.random.default_rng(3)
+    c = rng.normal(size=(pr.M, pr.P)).astype(np.float32)
+    c[1] += 1.0
+    A, d, _ = assemble(pr, c, rng.normal(size=pr.P), rng.normal(size=pr.P))
+    with pytest.raises(RuntimeError):
+        solve_normal(A, A.T @ d, method="cg", maxiter=3)
+    info = {}
+    solve_normal(A, A.T @ d, method="cg", maxiter=3, info=info, strict=False)
+    assert info["iters"] == 3 and info["rel_res"] > 1e-6
+    x = solve_normal(A, A.T @ d, method="cg")
+    assert np.allclose(x, solve_normal(A, A.T @ d, method="dense"), rtol=0, atol=1e-8 * np.abs(x).max())

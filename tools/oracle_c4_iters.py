@@ -19,7 +19,7 @@ out = {"config": "C4 PDE 0", "assembly_s": ta}
 for name, rhs in (("fwd", A.T @ d), ("bwd", g[0].reshape(-1).astype(np.float64))):
     info = {}
     t1 = time.perf_counter()
-    solve_normal(A, rhs, method="cg", tol=1e-12, maxiter=100000, info=info)
+    solve_normal(A, rhs, method="cg", tol=1e-12, maxiter=100000, info=info, strict=False)
     out[name] = {"iters": info["iters"], "rel_res": info["rel_res"], "seconds": time.perf_counter() - t1}
     print(name, out[name], flush=True)
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
