@@ -112,7 +112,9 @@ typedef struct {
                          the fixed SPD V-cycle), 1 = FGMRES(restart) with the same V-cycle as a
                          flexible right preconditioner -- the paper's method (SURVEY
                          §8(f) N1); its |g_{j+1}| is the true residual ||rt - S x||, so the same
-                         tol_inner / tol_inner2 / max_iters apply                           */
+                         tol_inner / max_iters apply; every refinement pass runs to
+                         min(tol_inner, tol_inner2) (GMRES minimises the residual, not the
+                         error: the PCG-calibrated tol_inner2 left e_z 1.5e-4 at C2)       */
   int32_t restart;    /* FGMRES restart length m, 1..32 (default 30; workspace grows by
                          (2m+1) scalar fields per PDE)                                      */
 } mpde_options;

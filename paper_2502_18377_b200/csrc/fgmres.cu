@@ -66,24 +66,43 @@ __global__ void __launch_bounds__(kThreads) k_gm_mdot(int P, int j1, int m1, con
   }
 }
 
-// w -= sum_{i < j1} coef[v][i] V_i ; part[(v*(m+1)) * nt + tile] = ||w||^2 over the tile
+// w -= sum_{i < j1} coef[v][i] V_i ; part[(v*(m+1)) * nt + tile] = ||w||^2 over the tile.
+// w stays in registers (kPer points per thread); per basis vector one coefficient load and
+// kPer independent coalesced loads (memory-level parallelism instead of a per-point chain).
 __global__ void __launch_bounds__(kThreads) k_gm_update(int P, int j1, int m1, const float* V,
                                                         size_t BP, const double* coef, float* w,
                                                         double* part, const int* act) {
   MPDE_PDL_ENTRY();
+  constexpr int kPer = kGmTile / kThreads;
   const int v = blockIdx.y;
   if (act && !act[v]) return;
   const int nt = gridDim.x;
-  const int p0 = blockIdx.x * kGmTile;
-  const int p1 = min(P, p0 + kGmTile);
+  const int p0 = blockIdx.x * kGmTile + threadIdx.x;
   float* wv = w + (size_t)v * P;
   const double* cv = coef + (size_t)v * m1;
+  float a[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int p = p0 + k * kThreads;
+    a[k] = p < P ? wv[p] : 0.f;
+  }
+  for (int i = 0; i < j1; ++i) {
+    const float c = float(cv[i]);
+    const float* Vi = V + i * BP + (size_t)v * P;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int p = p0 + k * kThreads;
+      if (p < P) a[k] -= c * Vi[p];
+    }
+  }
   double d = 0.0;
-  for (int p = p0 + threadIdx.x; p < p1; p += kThreads) {
-    float a = wv[p];
-    for (int i = 0; i < j1; ++i) a -= float(cv[i]) * V[i * BP + (size_t)v * P + p];
-    wv[p] = a;
-    d += double(a) * a;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int p = p0 + k * kThreads;
+    if (p < P) {
+      wv[p] = a[k];
+      d += double(a[k]) * a[k];
+    }
   }
   d = gm_block_sum(d);
   if (threadIdx.x == 0) part[(size_t)v * m1 * nt + blockIdx.x] = d;
@@ -119,20 +138,38 @@ __global__ void __launch_bounds__(kThreads) k_gm_resid(int P, int m1, const floa
   if (threadIdx.x == 0) part[(size_t)v * m1 * nt + blockIdx.x] = d;
 }
 
-// x += sum_{i < k[v]} y_i Z_i  for the PDEs of the cycle (gact)
+// x += sum_{i < k[v]} y_i Z_i  for the PDEs of the cycle (gact); register tile as k_gm_update
 __global__ void __launch_bounds__(kThreads) k_gm_xupdate(int P, int m1, const float* Z, size_t BP,
                                                          const double* y, const int* k, float* x,
                                                          const int* gact) {
   MPDE_PDL_ENTRY();
+  constexpr int kPer = kGmTile / kThreads;
   const int v = blockIdx.y;
   if (!gact[v]) return;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P) return;
+  const int p0 = blockIdx.x * kGmTile + threadIdx.x;
   const int kv = k[v];
   const double* yv = y + (size_t)v * m1;
-  float a = x[(size_t)v * P + p];
-  for (int i = 0; i < kv; ++i) a += float(yv[i]) * Z[i * BP + (size_t)v * P + p];
-  x[(size_t)v * P + p] = a;
+  float* xv = x + (size_t)v * P;
+  float a[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int p = p0 + q * kThreads;
+    a[q] = p < P ? xv[p] : 0.f;
+  }
+  for (int i = 0; i < kv; ++i) {
+    const float c = float(yv[i]);
+    const float* Zi = Z + i * BP + (size_t)v * P;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int p = p0 + q * kThreads;
+      if (p < P) a[q] += c * Zi[p];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int p = p0 + q * kThreads;
+    if (p < P) xv[p] = a[q];
+  }
 }
 
 // one CTA per PDE: warps reduce the per-tile partials of the j1 values (fixed order), thread 0
@@ -266,7 +303,7 @@ void launch_gm_resid(int P, int B, int m, const float* rt, float* y, int first, 
 void launch_gm_xupdate(int P, int B, int m, const float* Z, const GmState& g, float* x,
                        cudaStream_t s) {
   ++g_launch_count;
-  k_gm_xupdate<<<dim3((P + kThreads - 1) / kThreads, B), kThreads, 0, s>>>(
+  k_gm_xupdate<<<dim3(gm_tiles(P), B), kThreads, 0, s>>>(
       P, m + 1, Z, (size_t)B * P, g.coef, g.k, x, g.gact);
 }
 void launch_gm_scalar(int op, int j, int m, int P, int B, const PdeState& st, const GmState& g,
