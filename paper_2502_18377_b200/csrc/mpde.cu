@@ -1001,7 +1001,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
   h->st.tol_z = opts->tol_z;
   {
     // FGMRES minimises the residual, not the S-norm error: at C2 (ill-conditioned) its passes
-    // >= 2 at tol_inner2 = 3e-3 left e_z = 1.5e-4 (PCG 1.2e-6; gpurun_out/s7_c2.log), so with
+    // >= 2 at tol_inner2 = 3e-3 left e_z = 1.5e-4 (PCG 1.2e-6; profiles/r1s4_fgmres_c2_tol.txt), so with
     // krylov = 1 every pass runs to min(tol_inner, tol_inner2) (C2 e_z 2.9e-5; Q14)
     const float t2 = opts->krylov == 1 ? std::min(opts->tol_inner, opts->tol_inner2) : opts->tol_inner2;
     h->st.tol2_later = t2 * t2;
