@@ -538,6 +538,43 @@ __global__ void __launch_bounds__(kThreads) k_smooth_start4(int P4, const float4
   e[o] = dv;
 }
 
+// float4 k_pcg_update: one CTA covers 4 of the 1-point kernel's 256-point tiles and writes
+// their 4 partials into the same slots (part[v * ntiles(P) + tile]), so the consumers'
+// partial count and layout are unchanged
+__global__ void __launch_bounds__(kThreads) k_pcg_update4(int P4, int nt,
+                                                         const float* __restrict__ alpha,
+                                                         const float4* __restrict__ p_,
+                                                         const float4* __restrict__ q, float4* x,
+                                                         float4* r, double* part, const int* act) {
+  MPDE_PDL_ENTRY();
+  __shared__ double sh[kThreads / 32];
+  const int v = blockIdx.y;
+  if (act && !act[v]) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  double dot = 0.0;
+  if (p < P4) {
+    const size_t o = (size_t)v * P4 + p;
+    const float a = alpha[v];
+    const float4 pv = p_[o], qv = q[o];
+    float4 xv = x[o], rv = r[o];
+    xv.x += a * pv.x; xv.y += a * pv.y; xv.z += a * pv.z; xv.w += a * pv.w;
+    rv.x -= a * qv.x; rv.y -= a * qv.y; rv.z -= a * qv.z; rv.w -= a * qv.w;
+    x[o] = xv;
+    r[o] = rv;
+    dot = double(rv.x) * rv.x + double(rv.y) * rv.y + double(rv.z) * rv.z + double(rv.w) * rv.w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = dot;
+  __syncthreads();
+  // tile k of this CTA = float4 indices [64k, 64k + 64) = warps 2k, 2k + 1
+  constexpr int kSub = kThreads / 64;
+  if (threadIdx.x < kSub) {
+    const int tile = blockIdx.x * kSub + threadIdx.x;
+    if (tile < nt) part[(size_t)v * nt + tile] = sh[2 * threadIdx.x] + sh[2 * threadIdx.x + 1];
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_p_update4(int P4, const float* __restrict__ beta,
                                                        const float4* __restrict__ z, float4* p_,
                                                        const int* act) {
@@ -1083,6 +1120,12 @@ void launch_smooth_start(int P, int nvec, const float* r, const float* dinv, con
 void launch_pcg_update(int P, int nvec, const float* alpha, const float* p, const float* q,
                        float* x, float* r, double* part, const int* act, cudaStream_t s) {
   ++g_launch_count;
+  if (vec4_ok(P, p, q, x, r)) {
+    k_pcg_update4<<<grid_for(P / 4, nvec), kThreads, 0, s>>>(
+        P / 4, ntiles(P), alpha, (const float4*)p, (const float4*)q, (float4*)x, (float4*)r, part,
+        act);
+    return;
+  }
   k_pcg_update<<<grid_for(P, nvec), kThreads, 0, s>>>(P, alpha, p, q, x, r, part, act);
 }
 void launch_p_update(int P, int nvec, const float* beta, const float* z, float* p,
