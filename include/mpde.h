@@ -197,7 +197,12 @@ int mpde_apply_precond(mpde_hierarchy* h, const float* r, float* z, mpde_stream_
  *   what = 0: level shape (n0, n1, n2, levels) -> dst is HOST int32[4] (synchronous)
  *   what = 1: 1/diag(S_l) [B][P_l] fp32        what = 2: lambda_max [B] fp32
  *   what = 3: coarse coefficients [B][|M|][P_l] fp32
- *   what = 4: coarsest-level inverse [B][P_c][P_c] fp32 (level ignored) */
+ *   what = 4: coarsest-level inverse [B][P_c][P_c] fp32 (level ignored)
+ *   what = 5: kernel variants applying S on the level -> dst is HOST int32[4] (synchronous):
+ *             [pass 1 of the PCG operator, pass 2 of the PCG operator, pass 2 of the V-cycle
+ *             applies, 1 if those read bf16 coefficients]; codes 0 scalar, 1 v4, 2 v4
+ *             warp-specialised, 3 t-blocked, 4 t-blocked with compile-time extents,
+ *             5 2x2-blocked, 6 smem tile, 7 fused, 8 pass 1 with the y part */
 int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* dst,
                          mpde_stream_t stream);
 

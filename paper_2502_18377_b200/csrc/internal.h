@@ -134,6 +134,8 @@ void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaSt
 // bf16 per-point coefficients (cf16: [B][2+2D][P] __nv_bfloat16) for the V-cycle's applies
 // (epilogues RESID / SMOOTH / SMOOTH_LAST / POST0); only where schur_bf16_ok()
 bool schur_bf16_ok(const Geo& G, bool f64);
+// kernel variants applying S on a level (codes in schur.cu); mpde_hierarchy_query what = 5
+void schur_variants(const Geo& G, bool f64, bool bf16_level, int32_t out[4]);
 void launch_schur_g_bf(const Geo& G, int nvec, int crep, const void* cf16, const float* x, void* g,
                        const int* act, unsigned long long* pts, cudaStream_t s);
 void launch_schur_out_bf(int epi, const Geo& G, int nvec, int crep, const void* cf16,

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <string>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <vector>
 
@@ -254,9 +255,30 @@ void append_axis_tables(int n, double h, double wr, double ws, std::vector<float
   }
 }
 
+// Offsets are rounded to 256 bytes relative to the workspace base; the base itself is
+// first aligned up to 256 bytes, which the +256 slack of plan_workspace covers, so every
+// buffer is 256-byte aligned whatever the caller's workspace alignment (the S kernels do
+// unconditional 16-byte vector loads on cf / tab / x).
+// The per-axis tables depend only on (n, h, w_der, w_smooth): built once per process and
+// reused by every later hierarchy build (the fp64 host build was ~4% of a C4 step).
+const std::vector<float>& axis_tables_cached(int n, double hd, double wr, double ws) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, double, double, double>, std::vector<float>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(n, hd, wr, ws);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  std::vector<float>& t = cache[key];
+  append_axis_tables(n, hd, wr, ws, t);
+  return t;
+}
+
 struct Bump {
   char* base;
   size_t off = 0;
+  explicit Bump(char* b) : base(b) {
+    if (b) off = (256 - (reinterpret_cast<uintptr_t>(b) & 255)) & 255;
+  }
   template <typename T>
   T* take(size_t count) {
     off = (off + 255) & ~size_t(255);
@@ -341,7 +363,10 @@ struct mpde_hierarchy {
   char* ws_base;
   int* ones;     // [B] all 1
   float* rho;    // [B][P] equation residual b - c.z* of the last forward (fp64-derived)
-  const float* rho_b;  // rhs_b it was computed for
+  const float* rho_b = nullptr;  // rhs_b of the forward that wrote rho
+  const float* rho_z = nullptr;  // z output of that forward
+  unsigned long long fwd_gen = 0;  // forward calls on this handle
+  unsigned long long rho_gen = 0;  // generation of the forward that wrote rho
   // FGMRES (opts.krylov = 1): basis V [m+1][B][P], preconditioned basis Z [m][B][P]
   float *gmV = nullptr, *gmZ = nullptr;
   double* gmpart = nullptr;  // [B][m+1][gm_tiles(P)]
@@ -361,7 +386,7 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
   const int L = plan_levels(pr, op, shp);
   const int B = pr->batch, D = pr->ndim, M = 1 + 2 * D;
   const int P = shp[0].P, Pc = shp[L - 1].P;
-  Bump bp{base};
+  Bump bp(base);
   mpde_hierarchy tmp;
   mpde_hierarchy* h = H ? H : &tmp;
   int scale[kMaxD] = {1, 1, 1};
@@ -601,14 +626,71 @@ int poll_active(mpde_hierarchy* h, cudaStream_t s, int* nact) {
   return MPDE_OK;
 }
 
-// CUDA graph of `k` PCG iterations, cached per (workspace base, problem, options): a
-// hierarchy rebuilt in the same workspace for the same problem has identical device
-// pointers and kernel parameters, so the instantiated graph stays valid across builds.
-// Captured on a private stream (the legacy default stream cannot be captured); the
-// graph is launched on the caller's stream.
+// CUDA graph of `k` PCG iterations, cached per (device, aligned workspace base, problem,
+// options, k): a hierarchy rebuilt in the same workspace for the same problem has identical
+// device pointers and kernel parameters (the iterations touch only workspace buffers), so
+// the instantiated graph stays valid across builds.  The key is built from the named
+// fields (never raw struct bytes, whose padding a C caller may leave uninitialised).  At
+// most kGraphCacheMax graphs are kept; the least recently used one is destroyed when a new
+// one is captured (callers that allocate a fresh workspace per call no longer leak).
+// Captured on a private stream (the legacy default stream cannot be captured); the graph
+// is launched on the caller's stream.
+constexpr size_t kGraphCacheMax = 16;
+struct GraphEntry {
+  cudaGraphExec_t exec;
+  unsigned long long nodes;
+  unsigned long long last_use;
+  int device;
+};
 std::mutex g_graph_mu;
-std::map<std::string, std::pair<cudaGraphExec_t, unsigned long long>> g_graphs;
+std::map<std::string, GraphEntry> g_graphs;
+unsigned long long g_graph_clock = 0;
 cudaStream_t g_capture_stream = nullptr;
+int g_capture_device = -1;
+
+template <typename T>
+static void key_put(std::string& k, const T& v) {
+  k.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+static std::string graph_key(const mpde_hierarchy* h, int k, int device) {
+  std::string key;
+  key_put(key, device);
+  key_put(key, reinterpret_cast<uintptr_t>(h->lv[0].cf));  // aligned workspace base
+  key_put(key, k);
+  const mpde_problem& p = h->prob;
+  key_put(key, p.ndim);
+  for (int d = 0; d < p.ndim; ++d) {
+    key_put(key, p.n[d]);
+    key_put(key, p.h[d]);
+  }
+  key_put(key, p.batch);
+  key_put(key, p.deriv_order);
+  key_put(key, p.w_eq);
+  key_put(key, p.w_bnd);
+  key_put(key, p.w_deriv);
+  key_put(key, p.w_smooth);
+  const mpde_options& o = h->opts;
+  key_put(key, o.tol);
+  key_put(key, o.tol_inner);
+  key_put(key, o.max_iters);
+  key_put(key, o.max_refine);
+  key_put(key, o.smoother);
+  key_put(key, o.nu);
+  key_put(key, o.coarsest);
+  key_put(key, o.levels_max);
+  key_put(key, o.poll_every);
+  key_put(key, o.jacobi_theta);
+  key_put(key, o.cheb_ratio);
+  key_put(key, o.lanczos_steps);
+  key_put(key, o.precision);
+  key_put(key, o.use_graphs);
+  key_put(key, o.tol_z);
+  key_put(key, o.tol_inner2);
+  key_put(key, o.cf_bf16);
+  key_put(key, o.krylov);
+  key_put(key, o.restart);
+  return key;
+}
 
 // Programmatic dependent launch inside the PCG graphs (env MPDE_PDL, default 1): every
 // kernel -> kernel edge of the captured chain becomes a programmatic edge, so the next
@@ -649,17 +731,33 @@ static int make_edges_programmatic(cudaGraph_t graph) {
 template <class F>
 int chunk_graph(mpde_hierarchy* h, int k, F& iteration, cudaGraphExec_t* out,
                 unsigned long long* nodes) {
-  std::string key((const char*)&h->ws_base, sizeof(h->ws_base));
-  key.append((const char*)&h->prob, sizeof(h->prob));
-  key.append((const char*)&h->opts, sizeof(h->opts));
+  int device = 0;
+  CK(cudaGetDevice(&device));
+  const std::string key = graph_key(h, k, device);
   std::lock_guard<std::mutex> lock(g_graph_mu);
   auto it = g_graphs.find(key);
   if (it != g_graphs.end()) {
-    *out = it->second.first;
-    *nodes = it->second.second;
+    it->second.last_use = ++g_graph_clock;
+    *out = it->second.exec;
+    *nodes = it->second.nodes;
     return MPDE_OK;
   }
-  if (!g_capture_stream) CK(cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking));
+  while (g_graphs.size() >= kGraphCacheMax) {  // evict the least recently used graph
+    auto lru = g_graphs.begin();
+    for (auto i = g_graphs.begin(); i != g_graphs.end(); ++i)
+      if (i->second.last_use < lru->second.last_use) lru = i;
+    int cur = device;
+    if (lru->second.device != cur) CK(cudaSetDevice(lru->second.device));
+    CK(cudaDeviceSynchronize());  // an evicted graph may still be running on some stream
+    cudaGraphExecDestroy(lru->second.exec);
+    if (lru->second.device != cur) CK(cudaSetDevice(cur));
+    g_graphs.erase(lru);
+  }
+  if (g_capture_stream && g_capture_device != device) g_capture_stream = nullptr;
+  if (!g_capture_stream) {
+    CK(cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking));
+    g_capture_device = device;
+  }
   cudaGraph_t graph = nullptr;
   const unsigned long long l0 = g_launch_count.load();
   CK(cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeThreadLocal));
@@ -693,7 +791,7 @@ int chunk_graph(mpde_hierarchy* h, int k, F& iteration, cudaGraphExec_t* out,
   cudaGraphDestroy(graph);
   if (e2 != cudaSuccess)
     return set_err(MPDE_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2));
-  g_graphs[key] = {exec, n};
+  g_graphs[key] = GraphEntry{exec, n, ++g_graph_clock, device};
   *out = exec;
   *nodes = n;
   return MPDE_OK;
@@ -1022,8 +1120,10 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
     Level& lv = h->lv[l];
     // per-axis row tables of S (host, fp64 -> fp32) and per-point coefficients
     lv.tab_host.clear();
-    for (int d = 0; d < h->prob.ndim; ++d)
-      append_axis_tables(lv.G.n[d], lv.G.hd[d], lv.G.wr, lv.G.ws, lv.tab_host);
+    for (int d = 0; d < h->prob.ndim; ++d) {
+      const std::vector<float>& t = axis_tables_cached(lv.G.n[d], lv.G.hd[d], lv.G.wr, lv.G.ws);
+      lv.tab_host.insert(lv.tab_host.end(), t.begin(), t.end());
+    }
     CK(cudaMemcpyAsync(lv.tab, lv.tab_host.data(), sizeof(float) * lv.tab_host.size(),
                        cudaMemcpyHostToDevice, s));
     for (int d = 0; d < h->prob.ndim; ++d) {  // interior rows -> kernel params
@@ -1114,6 +1214,8 @@ int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, floa
   if (int rc = solve_core(h, nullptr, rhs_b, bnd, s)) return rc;
   PROF(10, s, launch_fwd_out(h->lv[0].G, B, h->lv[0].c, rhs_b, h->z64, z, h->rho, s));
   h->rho_b = rhs_b;
+  h->rho_z = z;
+  h->rho_gen = ++h->fwd_gen;
   if (stats) launch_stats_out(B, h->st, stats, s);
   CKL();
   return MPDE_OK;
@@ -1128,7 +1230,11 @@ int mpde_solve_bwd(mpde_hierarchy* h, const float* rhs_b, const float* z, const 
   const int B = h->B;
   Level& l0 = h->lv[0];
   if (int rc = solve_core(h, g_z, nullptr, nullptr, s)) return rc;
-  PROF(10, s, launch_grad(l0.G, B, l0.c, rhs_b, z, h->rho_b == rhs_b ? h->rho : nullptr, h->z64,
+  // rho kept by the last forward on this handle is used only for the same (rhs_b, z) pair;
+  // any other pair (or no forward yet) forms b - c.z from the fp32 z instead
+  const bool rho_ok = h->rho_gen != 0 && h->rho_gen == h->fwd_gen && h->rho_b == rhs_b &&
+                      h->rho_z == z;
+  PROF(10, s, launch_grad(l0.G, B, l0.c, rhs_b, z, rho_ok ? h->rho : nullptr, h->z64,
                           grad_coeff, grad_rhs, grad_bnd, dz_opt, s));
   if (stats) launch_stats_out(B, h->st, stats, s);
   CKL();
@@ -1181,6 +1287,12 @@ int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* d
     case 0: {
       int32_t shp[4] = {lv.G.n[0], lv.G.n[1], h->prob.ndim > 2 ? lv.G.n[2] : 0, h->L};
       std::memcpy(dst, shp, sizeof(shp));
+      return MPDE_OK;
+    }
+    case 5: {  // host int32[4]: kernel variants applying S on this level (schur.cu codes)
+      int32_t v[4];
+      schur_variants(lv.G, f64_pcg(h), lv.cf16 != nullptr, v);
+      std::memcpy(dst, v, sizeof(v));
       return MPDE_OK;
     }
     case 1:
@@ -1320,7 +1432,7 @@ int mpde_fwd_bwd_host(const mpde_problem* prob, const mpde_options* opts, const 
   size_t P = 1;
   for (int d = 0; d < prob->ndim; ++d) P *= prob->n[d];
   const size_t B = prob->batch, M = 1 + 2 * prob->ndim;
-  Bump bp{(char*)device_staging};
+  Bump bp((char*)device_staging);
   float* c = bp.take<float>(B * M * P);
   float* g = bp.take<float>(B * M * P);
   float* z = bp.take<float>(B * M * P);

@@ -2075,6 +2075,31 @@ void launch_schur_fused(int epi, const Geo& G, int nvec, int crep, const float* 
 #undef FUSED_CASE
 }
 
+// Kernel variants that apply S on a level (mpde_hierarchy_query what = 5; the tests assert the
+// selection so that a parity case really exercises the kernel it names):
+//   out[0] pass 1 of the PCG operator, out[1] pass 2 of the PCG operator,
+//   out[2] pass 2 of the V-cycle applies, out[3] 1 if those read bf16 coefficients.
+// Codes: 0 scalar, 1 v4, 2 v4 warp-specialised, 3 t-blocked (runtime extents),
+// 4 t-blocked (compile-time extents), 5 2x2-blocked, 6 smem tile, 7 fused, 8 pass 1 with y part.
+static int pass2_kind(const Geo& G, bool f64) {
+  if (use_fused(G, f64)) return 7;
+  if (use_tile(G, f64)) return 6;
+  if (use_b22(G, f64)) {
+    if (block_mode() == 2) return 5;
+    const bool ct = (G.n[1] == G.n[2]) && (G.n[2] == 32 || G.n[2] == 64 || G.n[2] == 128);
+    return ct ? 4 : 3;
+  }
+  if (use_v4(G)) return use_remap(G) ? 2 : 1;
+  return 0;
+}
+void schur_variants(const Geo& G, bool f64, bool bf16_level, int32_t out[4]) {
+  out[0] = use_fused(G, f64) ? 7 : use_hy(G, f64) ? 8 : use_v4(G) ? 1 : 0;
+  out[1] = pass2_kind(G, f64);
+  const bool bf = bf16_level && schur_bf16_ok(G, f64);
+  out[2] = bf ? (use_b22(G, false) ? pass2_kind(G, false) : (use_remap(G) ? 2 : 1)) : pass2_kind(G, f64);
+  out[3] = bf ? 1 : 0;
+}
+
 void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaStream_t s) {
   ++g_launch_count;
   DISPATCH_D2(G.D, k_schur_diag<DD><<<grid2(G.P, B), kThreads, 0, s>>>(G, cf, dinv));

@@ -190,7 +190,7 @@ def mpde_apply_precond(h, r, z, stream=None):
 
 
 def mpde_hierarchy_query(h, level, what, dst, stream=None):
-    if what == 0:
+    if what in (0, 5):
         arr = (C.c_int32 * 4)()
         _check(lib().mpde_hierarchy_query(h, int(level), 0, C.cast(arr, C.c_void_p),
                                           _stream(stream)))

@@ -92,7 +92,7 @@ def test_template_terms_and_validation(mp):
 
 
 def test_fgmres_options_and_workspace(mp):
-    """krylov = 1 (FGMRES(m), §8(f) N1): default off, restart 20; the workspace grows by
+    """krylov = 1 (FGMRES(m), §8(f) N1): default off, restart 30; the workspace grows by
     (2m+1) scalar fields per PDE plus the per-PDE Arnoldi state; restart outside 1..32 and an
     unknown Krylov method are rejected (workspace 0)."""
     import ctypes as C

@@ -65,23 +65,34 @@ y = torch.empty(d["x"].shape, dtype=torch.float32, device="cuda")
 mpde.mpde_apply_schur(s.h_, 0, torch.from_numpy(d["x"]).cuda(), y)
 torch.cuda.synchronize()
 np.save(sys.argv[2], y.cpu().numpy())
+np.save(sys.argv[3], np.array(mpde.mpde_hierarchy_query(s.h_, 0, 5, None)))
 """
 
 
-@pytest.mark.parametrize("shape,h,env", [
-    ((7, 16, 32), (0.05, 0.06, 0.07), {"MPDE_FUSED": "1"}),   # fused, 2 x-tiles
-    ((9, 24, 36), (0.04, 0.03, 0.05), {"MPDE_FUSED": "1"}),   # fused, interior tile
-    ((7, 16, 64), (0.05, 0.06, 0.07), {}),                    # t-blocked pass 2, warp-specialised y (NY4=16)
-    ((8, 10, 32), (0.05, 0.06, 0.07), {}),                    # t-blocked pass 2, NY4=8 (4 interior / 4 edge)
-    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_HY": "1"}),      # y part in pass 1
-    ((9, 12, 32), (0.05, 0.06, 0.07), {"MPDE_HY": "1"}),
-    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_TILE": "1"}),    # smem-tiled pass 2
-    ((13, 12, 32), (0.05, 0.06, 0.07), {"MPDE_TILE": "1"}),   # partial last t tile
-    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_B22_TP": "4"})])  # t-pair CTA tiling
-def test_large_schur_matches_sparse(shape, h, env, tmp_path):
-    """S apply at n_y >= 32 through every 3D kernel variant (the selection switches are read
-    once per process, so the apply runs in a child process) against S applied through the
-    oracle's sparse A (no dense N at these sizes)."""
+# (shape, h, env, expected [pass 1, pass 2] kernel codes of mpde_hierarchy_query(what=5)):
+# levels above MPDE_SMALLP = 16384 points per vector select the production kernels; below it
+# the 64-thread v4 kernels run whatever the switches say, so the variant cases set
+# MPDE_SMALLP=0 and every case asserts the kernel that actually ran.
+_NOSMALL = {"MPDE_SMALLP": "0"}
+@pytest.mark.parametrize("shape,h,env,kinds", [
+    ((6, 64, 64), (0.01, 1 / 64, 1 / 64), {}, (1, 4)),        # C4 level-0 kernel <64,64> (production)
+    ((20, 32, 32), (0.02, 1 / 32, 1 / 32), {}, (1, 4)),       # C4 level-1 kernel <32,32> (production)
+    ((6, 128, 128), (0.005, 1 / 128, 1 / 128), {}, (1, 4)),   # C5 level-0 kernel <128,128>
+    ((17, 24, 48), (0.05, 0.06, 0.07), {}, (1, 3)),           # runtime extents (NY4 = 12, no remap)
+    ((7, 16, 32), (0.05, 0.06, 0.07), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7)),  # fused, 2 x-tiles
+    ((9, 24, 36), (0.04, 0.03, 0.05), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7)),  # fused, interior tile
+    ((7, 16, 64), (0.05, 0.06, 0.07), _NOSMALL, (1, 3)),      # t-blocked, warp-specialised y (NY4=16)
+    ((8, 10, 32), (0.05, 0.06, 0.07), _NOSMALL, (1, 3)),      # t-blocked, NY4=8 (4 interior / 4 edge)
+    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_HY": "1", **_NOSMALL}, (8, 3)),  # y part in pass 1
+    ((9, 12, 32), (0.05, 0.06, 0.07), {"MPDE_HY": "1", **_NOSMALL}, (8, 3)),
+    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_TILE": "1", **_NOSMALL}, (1, 6)),   # smem-tiled pass 2
+    ((13, 12, 32), (0.05, 0.06, 0.07), {"MPDE_TILE": "1", **_NOSMALL}, (1, 6)),  # partial last t tile
+    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_B22_TP": "4", **_NOSMALL}, (1, 3)),  # t-pair CTA tiling
+    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_SCHUR_BLOCK": "2", **_NOSMALL}, (1, 5))])  # 2x2 blocking
+def test_large_schur_matches_sparse(shape, h, env, kinds, tmp_path):
+    """S apply through every 3D kernel variant, incl. the production instantiations the
+    bench runs (the selection switches are read once per process, so the apply runs in a child
+    process), against S applied through the oracle's sparse A (no dense N at these sizes)."""
     import os
     import subprocess
     import sys
@@ -96,8 +107,10 @@ def test_large_schur_matches_sparse(shape, h, env, tmp_path):
     env = dict(os.environ, **env)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.run([sys.executable, "-c", _APPLY_SCRIPT, str(tmp_path / "in.npz"),
-                    str(tmp_path / "y.npy")], check=True, env=env, cwd=root)
+                    str(tmp_path / "y.npy"), str(tmp_path / "v.npy")], check=True, env=env, cwd=root)
     y = np.load(tmp_path / "y.npy")
+    v = np.load(tmp_path / "v.npy")
+    assert (int(v[0]), int(v[1])) == kinds, f"kernel variants {v.tolist()} != expected {kinds}"
     pr = Problem(shape, h, *w)
     for i in range(B):
         ref = _sparse_schur_apply(pr, c[i].astype(np.float64), x[i].astype(np.float64))
@@ -106,9 +119,12 @@ def test_large_schur_matches_sparse(shape, h, env, tmp_path):
 
 @pytest.mark.parametrize("shape,h", [((16, 18, 20), (0.05, 0.06, 0.07)), ((20, 24), (0.05, 0.04)),
                                      ((20, 32, 32), (0.05, 0.03, 0.03)),
+                                     ((6, 64, 64), (0.01, 1 / 64, 1 / 64)),
                                      ((64, 96), (0.05, 0.02))])
 def test_vcycle_symmetric_positive(shape, h):
-    """The V-cycle is a fixed SPD linear map (needed by PCG): <Ma, b> = <a, Mb>, <Ma, a> > 0."""
+    """The V-cycle is a fixed SPD linear map (needed by PCG): <Ma, b> = <a, Mb>, <Ma, a> > 0.
+    (20,32,32) and (6,64,64) run the level-0 V-cycle applies through the bf16-coefficient
+    t-blocked kernels <32,32> / <64,64> the bench uses (asserted)."""
     from paper_2502_18377_b200 import mpde
     rng = np.random.default_rng(6)
     D = len(shape)
@@ -116,6 +132,9 @@ def test_vcycle_symmetric_positive(shape, h):
     c = rng.normal(0.0, 0.5, (B, M, P))
     c[:, 1] += 1.0
     s = mpde.Solver(shape, h, torch.from_numpy(c.astype(np.float32)).cuda())
+    if P > 16384 and D == 3:
+        v = mpde.mpde_hierarchy_query(s.h_, 0, 5, None)
+        assert v[2] == 4 and v[3] == 1, v  # t-blocked <n,n> kernel reading bf16 coefficients
     a = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()
     b = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()
     ma, mb = torch.empty_like(a), torch.empty_like(b)

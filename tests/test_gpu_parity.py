@@ -280,3 +280,21 @@ def test_bwd_full_size_manufactured(gu):
             assert e_phi <= E_Z
         else:
             assert np.all(out["dz"][i] == 0.0)
+
+
+@pytest.mark.parametrize("max_iters,max_refine", [(3, 2), (500, 1)])
+def test_maxiter_status_reported(max_iters, max_refine, gu):
+    """A PDE that cannot meet the stop rule within the limits is flagged MAXITER (mpde.h
+    mpde_stats.status) and still gets a finite z: 3 PCG iterations per pass, or a single
+    refinement pass (the error-based stop needs >= 2 passes and the residual floor 1e-10 is out
+    of reach of one fp32 PCG pass)."""
+    from paper_2502_18377_b200 import mpde
+    bt = synth.make_batch("C3", 2)
+    cfg = bt["cfg"]
+    opts = mpde.mpde_default_options(max_iters=max_iters, max_refine=max_refine)
+    out = gu.gpu_solve(cfg.shape, cfg.h, bt["c"], bt["b"], bt["omega"], opts=opts)
+    for st in out["stats_fwd"]:
+        assert st["status"] == "maxiter", st
+        assert st["refines"] == max_refine
+        assert st["iters"] <= max_iters * max_refine
+    assert np.all(np.isfinite(out["z"]))
