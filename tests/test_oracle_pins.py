@@ -208,7 +208,7 @@ def test_hand_cases():
         assert np.allclose(A.T @ dlam, -np.array(case["g"]))  # Eq. 11 second block row
 
 
-@pytest.mark.parametrize("method", ["dense", "lu", "cg"])
+@pytest.mark.parametrize("method", ["dense", "lu", "cg", "slab"])
 def test_kkt_identities(method):
     """P5: A^T lambda* = 0 (Eq. 10 second block row, LS optimality) and lambda* = d - A z*."""
     cfg = synth.CONFIGS["C1"]
@@ -222,15 +222,23 @@ def test_kkt_identities(method):
 
 @pytest.mark.parametrize("shape,h", [((16, 16), (1 / 15, 1 / 15)), ((8, 8, 8), (0.1, 0.1, 0.1))])
 def test_solver_crosscheck(shape, h):
-    """P9: SVD-lstsq, equilibrated SuperLU + refinement and Jacobi-CG agree to 1e-9."""
+    """P9: SVD-lstsq, equilibrated SuperLU + refinement, Jacobi-CG and t-slab block-Jacobi
+    PCG agree to 1e-9 (forward), and the backward solves and field gradients of the dense and
+    slab methods agree to 1e-8 -- the slab method is what the C3 / C4 golden references use."""
     rng = np.random.default_rng(6)
     pr = Problem(shape, h)
     c = _rand_c(shape, rng)
     b = rng.normal(size=pr.P)
     om = rng.normal(size=pr.P)
-    zs = [solve_forward(pr, c, b, om, method=m)["z"] for m in ("dense", "lu", "cg")]
+    fs = [solve_forward(pr, c, b, om, method=m) for m in ("dense", "lu", "cg", "slab")]
+    zs = [f["z"] for f in fs]
     for z in zs[1:]:
         assert np.linalg.norm(z - zs[0]) <= 1e-9 * np.linalg.norm(zs[0])
+    g = rng.normal(size=pr.n_v)
+    bd = solve_backward(pr, fs[0], g, method="dense")
+    bs = solve_backward(pr, fs[3], g, method="slab")
+    for k in ("dz", "grad_c", "grad_b", "grad_omega"):
+        assert np.linalg.norm(bs[k] - bd[k]) <= 1e-8 * np.linalg.norm(bd[k]), k
 
 
 # ---------------------------------------------------------- P7 finite differences
@@ -367,3 +375,5 @@ def test_oracle_cg_refuses_unconverged():
     assert info["iters"] == 3 and info["rel_res"] > 1e-6
     x = solve_normal(A, A.T @ d, method="cg")
     assert np.allclose(x, solve_normal(A, A.T @ d, method="dense"), rtol=0, atol=1e-8 * np.abs(x).max())
+    with pytest.raises(RuntimeError):  # the slab method refuses too
+        solve_normal(A, A.T @ d, method="slab", maxiter=1, shape=pr.shape)
