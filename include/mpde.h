@@ -65,6 +65,10 @@ enum {
 enum { MPDE_STATUS_CONVERGED = 0, MPDE_STATUS_MAXITER = 1, MPDE_STATUS_NONFINITE = 2,
        MPDE_STATUS_INDEFINITE = 3 };
 
+/* boundary types per face (mpde_problem.bc): "Dirichlet (i.e., boundary conditions
+ * on u), Neumann (i.e., boundary conditions on partial derivatives) or mixed types" */
+enum { MPDE_BC_DIRICHLET = 0, MPDE_BC_NEUMANN = 1, MPDE_BC_NONE = 2 };
+
 /* Grid, batch and row-group weights.  P:89 (Cartesian grid), P:111-117 (uniform step
  * per dim -- learned per-interval steps are out of scope), P:147-151 (variables). */
 typedef struct {
@@ -74,6 +78,14 @@ typedef struct {
   int32_t batch;       /* B >= 1 independent PDEs                                        */
   int32_t deriv_order; /* must be 2: M = {phi, d_k, d_kk for every dim}                 */
   float   w_eq, w_bnd, w_deriv, w_smooth; /* row-group weights, > 0 (paper: all 1)      */
+  int32_t bc[4][2];    /* boundary type of face (dim d, low = 0 / high = 1 side), MPDE_BC_*:
+                          DIRICHLET: w_bnd u_phi(p) = w_bnd omega(p) on every point of the
+                            face (one row per point on at least one Dirichlet face);
+                          NEUMANN: w_bnd u_{d}(p) = w_bnd omega_n[d](p) (the first-derivative
+                            variable along the face's axis; one row per face point);
+                          NONE: no boundary row on that face.
+                          All zero (the default of a zero-initialised struct) = every face
+                          Dirichlet, the paper's Eq. 4 with B = all faces (reading Q1).  */
 } mpde_problem;
 
 /* Solver options.  The Krylov method is PCG on the (condensed) normal equations; the
@@ -130,7 +142,8 @@ typedef struct {
 
 typedef struct mpde_hierarchy mpde_hierarchy; /* opaque, host-side handle */
 
-/* Defaults: tol_z 1e-4 (measured errors 4-100x below it on C2-C4 and their MMS twins), tol 1e-10, tol_inner 3e-4, tol_inner2 3e-3, max_refine 6, Chebyshev nu = 2, coarsest 8,
+/* Defaults: tol_z 1e-5 (10x below the north_star bar 1e-4: the estimate can read up to ~8x
+ * low; on C2-C4 it costs no extra iterations, profiles/r2_tolz_sweep.txt), tol 1e-10, tol_inner 3e-4, tol_inner2 3e-3, max_refine 6, Chebyshev nu = 2, coarsest 8,
  * 16 Lanczos steps, precision 1. */
 mpde_options mpde_default_options(void);
 
@@ -158,10 +171,21 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts,
 int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, float* z,
                    mpde_stats* stats, mpde_stream_t stream);
 
+/* Forward / backward with Neumann data (faces of type MPDE_BC_NEUMANN):
+ * bnd_n [B][ndim][P] (device, read only on the Neumann faces of dim d; NULL = homogeneous
+ * Neumann data, omega_n = 0); grad_bnd_n [B][ndim][P] (device, written: dl/domega_n on the
+ * Neumann faces of dim d, 0 elsewhere; NULL = not computed).  mpde_solve_fwd / _bwd are these
+ * calls with NULL Neumann arguments. */
+int mpde_solve_fwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* bnd, const float* bnd_n,
+                      float* z, mpde_stats* stats, mpde_stream_t stream);
+int mpde_solve_bwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,
+                      float* grad_coeff, float* grad_rhs, float* grad_bnd, float* grad_bnd_n,
+                      float* dz_opt, mpde_stats* stats, mpde_stream_t stream);
+
 /* Backward pass (Eq. 11) for the loss gradient g_z = dl/dz* [B][|M|][P]:
  * solves A^T A d_z = g_z with the same hierarchy and writes
  *   grad_coeff[b][m][p] = dl/dc_m(p),  grad_rhs[b][p] = dl/db(p),
- *   grad_bnd[b][p] = dl/domega(p) (0 off the boundary set),  dz_opt = d_z (or NULL).
+ *   grad_bnd[b][p] = dl/domega(p) (0 off the Dirichlet faces),  dz_opt = d_z (or NULL).
  * z must be the forward solution for the same rhs_b.  If the last mpde_solve_fwd on this
  * handle was called with the same rhs_b pointer, the equation residual b - c.z* it kept
  * (formed from its fp64 solution) is used for grad_coeff; otherwise it is formed from the
@@ -264,14 +288,17 @@ int mpde_template_grad(const mpde_problem* prob, const mpde_template* t, const f
 /* ---- launch profiler (process-wide, not thread-safe; off by default) ------------
  * Between begin and end every library launch is bracketed by CUDA events on the
  * stream it is launched on.  end() synchronises and returns, per launch class,
- * the summed event time (ms) and the launch count; pts[0..6] = points processed by the
- * S pass-2 kernel per epilogue kind on levels >= 1, pts[9..15] the same on level 0,
- * pts[8] / pts[7] = points processed by the S pass-1 kernel on levels >= 1 / level 0.
+ * the summed event time (ms) and the launch count, and pts[0..31], points processed:
+ * pts[0..6] by the S pass-2 kernel per epilogue kind on levels >= 1, pts[9..15] the same on
+ * level 0, pts[8] / pts[7] by the S pass-1 kernel on levels >= 1 / level 0, pts[16..22] by
+ * the one-kernel t-marching S apply per epilogue kind on level 0, pts[24..30] the same on
+ * levels >= 1.
  * Classes: 0 S pass 1 (schur_g, levels >= 1), 1 S pass 2 (schur_out, levels >= 1),
  * 2 fp64 residual, 3 condense, 4 back-substitution, 5 grid transfers, 6 PCG/smoother
  * vector ops, 7 per-PDE scalar logic, 8 coarsest solve, 9 hierarchy build,
- * 10 forward/backward epilogues, 11 S pass 2 on level 0, 12 S pass 1 on level 0. */
-#define MPDE_PROF_NCLASS 13
+ * 10 forward/backward epilogues, 11 S pass 2 on level 0, 12 S pass 1 on level 0,
+ * 13 t-marching S apply on level 0, 14 t-marching S apply on levels >= 1. */
+#define MPDE_PROF_NCLASS 15
 /* Number of kernel launches this process has issued through the library so far. */
 uint64_t mpde_launch_count(void);
 int mpde_profile_begin(void);

@@ -45,7 +45,20 @@ struct Geo {
   // interior rows of the tables (identical for 7 <= i <= n-8), kept in the constant bank:
   // [0,10) Kf o=-2..2 x k, [10,20) KT o=-2..2 x k, [20,29) P0 o=-4..4
   float irow[kMaxD][32];
+  // boundary types per face (mpde_problem.bc): 0 Dirichlet, 1 Neumann, 2 none;
+  // nb2 = w_bnd^2 on the Neumann faces (the Neumann row's N_dd entry), 0 otherwise
+  int bc[kMaxD][2];
+  float nb2[kMaxD][2];
 };
+
+// point index i of axis d lies on a Dirichlet face (Eq. 4 rows; reading Q1 / B1)
+__device__ __forceinline__ bool dir_face(const Geo& G, int d, int i) {
+  return (i == 0 && G.bc[d][0] == 0) || (i == G.n[d] - 1 && G.bc[d][1] == 0);
+}
+// w_bnd^2 of the Neumann row(s) of the first-derivative variable along d at index i
+__device__ __forceinline__ float neu_w2(const Geo& G, int d, int i) {
+  return (i == 0 ? G.nb2[d][0] : 0.f) + (i == G.n[d] - 1 ? G.nb2[d][1] : 0.f);
+}
 
 // 5-point FD weights for the unit-spaced grid, per class and ascending offset.
 // class 0,1: forward (offsets 0..4), 2: central (-2..2), 3,4: backward (-4..0).
@@ -59,13 +72,15 @@ __device__ __forceinline__ int fd_cls(int i, int n) {
 __device__ __forceinline__ int fd_start(int cls) { return cls < 2 ? 0 : (cls == 2 ? -2 : -4); }
 
 // 2x2 block T_d(i) of N_dd from derivative + smoothness rows along axis d at index i:
-//   T11 = wr^2 h^2 + ws^2 h^2 (f+b), T12 = ws^2 h^3/2 (f-b), T22 = wr^2 h^4 + ws^2 h^4/4 (f+b)
-// with f = [i <= n-2] (forward row present), b = [i >= 1] (backward row present).
+//   T11 = wr^2 h^2 + ws^2 h^2 (f+b) + nb, T12 = ws^2 h^3/2 (f-b), T22 = wr^2 h^4 + ws^2 h^4/4 (f+b)
+// with f = [i <= n-2] (forward row present), b = [i >= 1] (backward row present) and nb the
+// w_bnd^2 of a Neumann row on the first-derivative variable (neu_w2).
 template <typename T>
-__device__ __forceinline__ void tinv(T h, T wr, T ws, bool f, bool b, T& t11, T& t12, T& t22) {
+__device__ __forceinline__ void tinv(T h, T wr, T ws, bool f, bool b, T& t11, T& t12, T& t22,
+                                     T nb = T(0)) {
   T h2 = h * h;
   T fb = T(f) + T(b), fmb = T(f) - T(b);
-  T a11 = wr * wr * h2 + ws * ws * h2 * fb;
+  T a11 = wr * wr * h2 + ws * ws * h2 * fb + nb;
   T a12 = ws * ws * h2 * h * T(0.5) * fmb;
   T a22 = wr * wr * h2 * h2 + ws * ws * h2 * h2 * T(0.25) * fb;
   T det = a11 * a22 - a12 * a12;
@@ -89,11 +104,12 @@ __device__ __forceinline__ void unravel(const Geo& G, int p, int* idx) {
   }
 }
 
+// the point carries a Dirichlet row: it lies on at least one Dirichlet face
 template <int D>
 __device__ __forceinline__ bool on_boundary(const Geo& G, const int* idx) {
   bool onb = false;
 #pragma unroll
-  for (int d = 0; d < D; ++d) onb |= (idx[d] == 0) | (idx[d] == G.n[d] - 1);
+  for (int d = 0; d < D; ++d) onb |= dir_face(G, d, idx[d]);
   return onb;
 }
 

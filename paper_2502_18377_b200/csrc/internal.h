@@ -107,8 +107,8 @@ void upload_constants();
 void launch_rhs_init(const Geo& G, int B, const float* c, const float* b, const float* om,
                      float* rhs, double* part, cudaStream_t s);
 void launch_residual64(const Geo& G, int B, const float* c, const float* rhs, const float* b,
-                       const float* om, const double* z64, float* r, double* part, const int* act,
-                       cudaStream_t s);
+                       const float* om, const float* omn, const double* z64, float* r, double* part,
+                       const int* act, cudaStream_t s);
 void launch_apply_normal(const Geo& G, int B, const float* c, const float* z, float* q,
                          cudaStream_t s);
 void launch_ndd_solve(const Geo& G, int B, const float* c, const float* r, float* t,
@@ -125,9 +125,15 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* c,
 // schur.cu: cf = per-point coefficients [B][2+2D][P] of S (from c), dinv = 1/diag(S)
 void launch_schur_coef(const Geo& G, int B, const float* c, float* cf, cudaStream_t s);
 // number of CTAs (= partial sums per vector) of the S kernels on this level
-int schur_tiles(const Geo& G, bool f64);
+// partial sums per vector written by the S apply that schur_apply selects for nvec vectors
+int schur_tiles(const Geo& G, bool f64, int nvec);
 // true when this level applies S with the single fused kernel (launch_schur_fused)
 bool schur_fused(const Geo& G, bool f64);
+// one-kernel t-marching S apply (march.cu): 3D fp32 levels with n_y in {32,64,128}, n_x = 8k
+bool use_march(const Geo& G, bool f64, int nvec);  // also needs 16-byte aligned x
+int march_ctas(const Geo& G);
+void launch_schur_march(int epi, const Geo& G, int nvec, int crep, const void* cf, bool bf16,
+                        const float* x, const EpiArgs& A, const int* act, cudaStream_t s);
 void launch_schur_fused(int epi, const Geo& G, int nvec, int crep, const float* cf,
                         const float* x, const EpiArgs& A, const int* act, cudaStream_t s);
 void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaStream_t s);
@@ -135,7 +141,7 @@ void launch_diag_schur(const Geo& G, int B, const float* cf, float* dinv, cudaSt
 // (epilogues RESID / SMOOTH / SMOOTH_LAST / POST0); only where schur_bf16_ok()
 bool schur_bf16_ok(const Geo& G, bool f64);
 // kernel variants applying S on a level (codes in schur.cu); mpde_hierarchy_query what = 5
-void schur_variants(const Geo& G, bool f64, bool bf16_level, int32_t out[4]);
+void schur_variants(const Geo& G, bool f64, bool bf16_level, int nvec, int32_t out[4]);
 void launch_schur_g_bf(const Geo& G, int nvec, int crep, const void* cf16, const float* x, void* g,
                        const int* act, unsigned long long* pts, cudaStream_t s);
 void launch_schur_out_bf(int epi, const Geo& G, int nvec, int crep, const void* cf16,
@@ -179,7 +185,7 @@ void launch_smooth_coef(int B, int nu, int kind, float theta, float ratio, const
                         float* coef, cudaStream_t s);
 void launch_grad(const Geo& G, int B, const float* c, const float* b, const float* z,
                  const float* rho, const double* dz64, float* gc, float* gb, float* gw,
-                 float* dz_out, cudaStream_t s);
+                 float* gwn, float* dz_out, cudaStream_t s);
 void launch_fwd_out(const Geo& G, int B, const float* c, const float* b, const double* z64,
                     float* z, float* rho, cudaStream_t s);
 void launch_d2f(size_t n, const double* a, float* b, cudaStream_t s);

@@ -77,7 +77,7 @@ __device__ __forceinline__ void normal_point(const Geo& G, const float* __restri
           out[0] -= wr * (T(cA[0][cls][j]) * R1 + T(cA[1][cls][j]) * R2);
       }
       if (WANT_D && di == 0) {
-        out[1 + 2 * d] += wr * h * R1;
+        out[1 + 2 * d] += wr * h * R1 + T(neu_w2(G, d, i)) * zd1;  // + Neumann row
         out[2 + 2 * d] += wr * h2 * R2;
       }
       if (sm) {
@@ -114,7 +114,7 @@ __device__ __forceinline__ void ndd_solve(const Geo& G, const float* __restrict_
     const int i = idx[d], n = G.n[d];
     T t11, t12, t22;
     tinv<T>(sizeof(T) == 8 ? T(G.hd[d]) : T(G.h[d]), T(G.wr), T(G.ws), i <= n - 2, i >= 1, t11, t12,
-            t22);
+            t22, T(neu_w2(G, d, i)));
     const T g1 = T(G.we) * T(cb[(1 + 2 * d) * P + p]), g2 = T(G.we) * T(cb[(2 + 2 * d) * P + p]);
     u[2 * d] = t11 * g1 + t12 * g2;
     u[2 * d + 1] = t12 * g1 + t22 * g2;
@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(kThreads) k_residual64(Geo G, const float* __r
                                                         const float* __restrict__ rhs,
                                                         const float* __restrict__ bb,
                                                         const float* __restrict__ om,
+                                                        const float* __restrict__ omn,
                                                         const double* __restrict__ z64,
                                                         float* __restrict__ r, double* part,
                                                         const int* act) {
@@ -192,15 +193,29 @@ __global__ void __launch_bounds__(kThreads) k_residual64(Geo G, const float* __r
       for (int m = 0; m < M; ++m) out[m] = 0.0;
     }
     double bv = 0.0, wv = 0.0;
+    double nv[D];  // Neumann data rows: w_bnd^2 omega_n[d] on the (d,1) slot
+#pragma unroll
+    for (int d = 0; d < D; ++d) nv[d] = 0.0;
     if (!rhs) {
       const double we = G.we, wb = G.wb;
       bv = we * we * double(bb[(size_t)v * P + p]);
       wv = on_boundary<D>(G, idx) ? wb * wb * double(om[(size_t)v * P + p]) : 0.0;
+      if (omn) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const float nw = neu_w2(G, d, idx[d]);
+          if (nw != 0.f) nv[d] = double(nw) * double(omn[((size_t)v * D + d) * P + p]);
+        }
+      }
     }
 #pragma unroll
     for (int m = 0; m < M; ++m) {
+      double extra = m == 0 ? wv : 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d)
+        if (m == 1 + 2 * d) extra += nv[d];
       const double rh = rhs ? double(rhs[((size_t)v * M + m) * P + p])
-                            : double(cb[m * P + p]) * bv + (m == 0 ? wv : 0.0);
+                            : double(cb[m * P + p]) * bv + extra;
       double rv = rh - out[m];
       r[((size_t)v * M + m) * P + p] = float(rv);
       nrm += rv * rv;
@@ -921,7 +936,8 @@ __global__ void __launch_bounds__(kThreads) k_grad(Geo G, const float* __restric
                                                   const float* __restrict__ rho_in,
                                                   const double* __restrict__ dz64,
                                                   float* __restrict__ gc, float* __restrict__ gb,
-                                                  float* __restrict__ gw, float* __restrict__ dz_out) {
+                                                  float* __restrict__ gw, float* __restrict__ gwn,
+                                                  float* __restrict__ dz_out) {
   MPDE_PDL_ENTRY();
   constexpr int M = 1 + 2 * D;
   const int v = blockIdx.y, P = G.P;
@@ -949,6 +965,11 @@ __global__ void __launch_bounds__(kThreads) k_grad(Geo G, const float* __restric
   }
   gb[(size_t)v * P + p] = float(we2 * gam);
   gw[(size_t)v * P + p] = on_boundary<D>(G, idx) ? float(double(G.wb) * G.wb * dd[0]) : 0.f;
+  if (gwn) {  // dl/domega_n[d] = w_bnd^2 d_z,(d,1) on the Neumann faces of dim d
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      gwn[((size_t)v * D + d) * P + p] = float(double(neu_w2(G, d, idx[d])) * dd[1 + 2 * d]);
+  }
 }
 
 // forward epilogue: z = float(z64), rho = b - c.z64 (fp64)
@@ -1056,10 +1077,10 @@ void launch_rhs_init(const Geo& G, int B, const float* c, const float* b, const 
   DISPATCH_D(G.D, k_rhs_init<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, b, om, rhs, part));
 }
 void launch_residual64(const Geo& G, int B, const float* c, const float* rhs, const float* b,
-                       const float* om, const double* z64, float* r, double* part, const int* act,
-                       cudaStream_t s) {
+                       const float* om, const float* omn, const double* z64, float* r, double* part,
+                       const int* act, cudaStream_t s) {
   ++g_launch_count;
-  DISPATCH_D(G.D, k_residual64<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, rhs, b, om, z64, r, part, act));
+  DISPATCH_D(G.D, k_residual64<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, rhs, b, om, omn, z64, r, part, act));
 }
 void launch_apply_normal(const Geo& G, int B, const float* c, const float* z, float* q,
                          cudaStream_t s) {
@@ -1177,9 +1198,9 @@ void launch_smooth_coef(int B, int nu, int kind, float theta, float ratio, const
 }
 void launch_grad(const Geo& G, int B, const float* c, const float* b, const float* z,
                  const float* rho, const double* dz64, float* gc, float* gb, float* gw,
-                 float* dz_out, cudaStream_t s) {
+                 float* gwn, float* dz_out, cudaStream_t s) {
   ++g_launch_count;
-  DISPATCH_D(G.D, k_grad<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, b, z, rho, dz64, gc, gb, gw, dz_out));
+  DISPATCH_D(G.D, k_grad<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, b, z, rho, dz64, gc, gb, gw, gwn, dz_out));
 }
 void launch_fwd_out(const Geo& G, int B, const float* c, const float* b, const double* z64,
                     float* z, float* rho, cudaStream_t s) {

@@ -80,6 +80,11 @@ int validate(const mpde_problem* pr, const mpde_options* op) {
   if (P > (1LL << 30)) return set_err(MPDE_ERR_SHAPE, "grid too large");
   if (!(pr->w_eq > 0 && pr->w_bnd > 0 && pr->w_deriv > 0 && pr->w_smooth > 0))
     return set_err(MPDE_ERR_INVALID_ARG, "row-group weights must be > 0");
+  for (int d = 0; d < pr->ndim; ++d)
+    for (int sd = 0; sd < 2; ++sd)
+      if (pr->bc[d][sd] < MPDE_BC_DIRICHLET || pr->bc[d][sd] > MPDE_BC_NONE)
+        return set_err(MPDE_ERR_INVALID_ARG, "bc[%d][%d] must be 0 (Dirichlet), 1 (Neumann) or 2 (none)",
+                       d, sd);
   if (op->smoother < 0 || op->smoother > 1)
     return set_err(MPDE_ERR_UNSUPPORTED, "smoother must be 0 (Jacobi) or 1 (Chebyshev)");
   if (op->cf_bf16 != 0 && op->cf_bf16 != 1)
@@ -157,6 +162,12 @@ Geo make_geo(const mpde_problem* pr, const LevelShape& s, int level_scale[kMaxD]
   G.wb = pr->w_bnd;
   G.wr = pr->w_deriv;
   G.ws = pr->w_smooth;
+  for (int d = 0; d < kMaxD; ++d)
+    for (int sd = 0; sd < 2; ++sd) {
+      // every level carries the fine level's boundary types (rediscretised coarse operators)
+      G.bc[d][sd] = d < G.D ? pr->bc[d][sd] : MPDE_BC_DIRICHLET;
+      G.nb2[d][sd] = G.bc[d][sd] == MPDE_BC_NEUMANN ? pr->w_bnd * pr->w_bnd : 0.f;
+    }
   return G;
 }
 
@@ -183,7 +194,11 @@ void fd_row(int k, int i, int n, int* off, double* w) {
 // Kc[k][i][o]: coefficient of phi(i+o) in the derivative-variable row (k,i) of N
 // (derivative rows, Eq. 5, and Taylor rows, Eqs. 6-7); T_i = N_dd block of axis d;
 // P0 = K_pp - sum_i' Kc(i')^T T_i'^-1 Kc(i').
-void append_axis_tables(int n, double h, double wr, double ws, std::vector<float>& out) {
+// nlo / nhi: w_bnd^2 of a Neumann row on the first-derivative variable at index 0 / n-1
+// (face type MPDE_BC_NEUMANN): it enters T_0 / T_{n-1} and through T^-1 the edge
+// rows of P0; K and the interior rows are unchanged.
+void append_axis_tables(int n, double h, double wr, double ws, double nlo, double nhi,
+                        std::vector<float>& out) {
   const double wr2 = wr * wr, ws2 = ws * ws;
   std::vector<double> Kc((size_t)2 * n * 9, 0.0), Ti((size_t)n * 4), A((size_t)2 * n * 9, 0.0);
   auto kc = [&](int k, int i, int o) -> double& { return Kc[((size_t)k * n + i) * 9 + o + 4]; };
@@ -210,7 +225,8 @@ void append_axis_tables(int n, double h, double wr, double ws, std::vector<float
       kc(0, i, -1) += ws2 * h;
       kc(1, i, -1) -= 0.5 * ws2 * h * h;
     }
-    const double a11 = wr2 * h * h + ws2 * h * h * (f + b), a12 = ws2 * h * h * h * 0.5 * (f - b);
+    const double a11 = wr2 * h * h + ws2 * h * h * (f + b) + (i == 0 ? nlo : 0.0) + (i == n - 1 ? nhi : 0.0);
+    const double a12 = ws2 * h * h * h * 0.5 * (f - b);
     const double a22 = wr2 * h * h * h * h + ws2 * h * h * h * h * 0.25 * (f + b);
     const double det = a11 * a22 - a12 * a12;
     Ti[i * 4 + 0] = a22 / det;
@@ -261,15 +277,16 @@ void append_axis_tables(int n, double h, double wr, double ws, std::vector<float
 // unconditional 16-byte vector loads on cf / tab / x).
 // The per-axis tables depend only on (n, h, w_der, w_smooth): built once per process and
 // reused by every later hierarchy build (the fp64 host build was ~4% of a C4 step).
-const std::vector<float>& axis_tables_cached(int n, double hd, double wr, double ws) {
+const std::vector<float>& axis_tables_cached(int n, double hd, double wr, double ws, double nlo,
+                                            double nhi) {
   static std::mutex mu;
-  static std::map<std::tuple<int, double, double, double>, std::vector<float>> cache;
+  static std::map<std::tuple<int, double, double, double, double, double>, std::vector<float>> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_tuple(n, hd, wr, ws);
+  auto key = std::make_tuple(n, hd, wr, ws, nlo, nhi);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   std::vector<float>& t = cache[key];
-  append_axis_tables(n, hd, wr, ws, t);
+  append_axis_tables(n, hd, wr, ws, nlo, nhi, t);
   return t;
 }
 
@@ -295,7 +312,10 @@ struct Prof {
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
   std::vector<int> cls;
-  unsigned long long* d_pts = nullptr;  // [8] points processed by k_schur_out per EPI, [8] k_schur_g
+  // [0,7) points processed by S pass 2 per EPI on levels >= 1, [7] pass 1 on level 0, [8] pass 1
+  // on levels >= 1, [9,16) pass 2 per EPI on level 0, [16,23) the t-marching S kernel per EPI on
+  // level 0, [24,31) the same on levels >= 1
+  unsigned long long* d_pts = nullptr;
 };
 Prof g_prof;
 
@@ -509,6 +529,17 @@ int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const flo
   // profiling: level 0 has its own classes (11 pass 2, 12 pass 1) and point counters
   A2.pts = g_prof.on ? g_prof.d_pts + (l == 0 ? 9 : 0) : nullptr;
   const int c_out = l == 0 ? 11 : 1, c_g = l == 0 ? 12 : 0;
+  // one-kernel t-marching S apply (march.cu): bulk-async plane streaming, DSMEM halo
+  // exchange; the V-cycle applies on level 0 read the bf16 coefficients (see below)
+  if (use_march(lv.G, f64, nvec) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0)) {
+    const bool bf = lv.cf16 && crep == 1 &&
+                    (epi == EPI_RESID || epi == EPI_SMOOTH || epi == EPI_SMOOTH_LAST || epi == EPI_POST0);
+    A2.pts = g_prof.on ? g_prof.d_pts + (l == 0 ? 16 : 24) : nullptr;
+    PROF(l == 0 ? 13 : 14, s,
+         launch_schur_march(epi, lv.G, nvec, crep, bf ? lv.cf16 : (const void*)cf, bf, x, A2, act, s));
+    CKL();
+    return MPDE_OK;
+  }
   if (schur_fused(lv.G, f64)) {
     PROF(c_out, s, launch_schur_fused(epi, lv.G, nvec, crep, cf, x, A2, act, s));
     CKL();
@@ -669,6 +700,10 @@ static std::string graph_key(const mpde_hierarchy* h, int k, int device) {
   key_put(key, p.w_bnd);
   key_put(key, p.w_deriv);
   key_put(key, p.w_smooth);
+  for (int d = 0; d < p.ndim; ++d) {
+    key_put(key, p.bc[d][0]);
+    key_put(key, p.bc[d][1]);
+  }
   const mpde_options& o = h->opts;
   key_put(key, o.tol);
   key_put(key, o.tol_inner);
@@ -705,6 +740,15 @@ static bool pdl_enabled() {
   return on != 0;
 }
 
+static bool is_cluster_node(cudaGraphNode_t n) {
+  cudaLaunchAttributeValue v{};
+  if (cudaGraphKernelNodeGetAttribute(n, cudaLaunchAttributeClusterDimension, &v) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return v.clusterDim.x * v.clusterDim.y * v.clusterDim.z > 1;
+}
+
 static int make_edges_programmatic(cudaGraph_t graph) {
   size_t ne = 0;
   CK(cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &ne));
@@ -717,6 +761,9 @@ static int make_edges_programmatic(cudaGraph_t graph) {
     CK(cudaGraphNodeGetType(from[i], &ta));
     CK(cudaGraphNodeGetType(to[i], &tb));
     if (ta != cudaGraphNodeTypeKernel || tb != cudaGraphNodeTypeKernel) continue;
+    // no programmatic edge next to a thread-block-cluster kernel (the t-marching S apply):
+    // early-launched CTAs of a neighbour kernel would hold the SMs its clusters need
+    if (is_cluster_node(from[i]) || is_cluster_node(to[i])) continue;
     if (ed[i].type == cudaGraphDependencyTypeProgrammatic) continue;
     CK(cudaGraphRemoveDependencies_v2(graph, &from[i], &to[i], &ed[i], 1));
     cudaGraphEdgeData pe{};
@@ -816,9 +863,9 @@ __global__ void k_dot_self(int P, const float* __restrict__ r, double* part, con
 int pcg(mpde_hierarchy* h, cudaStream_t s) {
   const int B = h->B, P = h->P;
   const int nt = ntiles(P);                  // partials of the pointwise vector kernels
-  const int nts = schur_tiles(h->lv[0].G, f64_pcg(h));   // partials of the PCG S kernel
+  const int nts = schur_tiles(h->lv[0].G, f64_pcg(h), h->B);   // partials of the PCG S kernel
   const int ntc = h->L == 1 ? coarse_gemv_blocks(h->Pc)  // ... of the V-cycle's last kernel
-                            : schur_tiles(h->lv[0].G, f64_vcycle(h));
+                            : schur_tiles(h->lv[0].G, f64_vcycle(h), h->B);
   const float tol2 = h->opts.tol_inner * h->opts.tol_inner;
   const int* act = h->st.act;
   Level& l0 = h->lv[0];
@@ -967,12 +1014,12 @@ int fgmres(mpde_hierarchy* h, cudaStream_t s) {
 // Solve N z = rhs for every PDE (refinement loop); result in h->z64.  rhs == nullptr:
 // rhs = A^T d from (b, om), formed in fp64 inside the residual kernel.
 int solve_core(mpde_hierarchy* h, const float* rhs, const float* b, const float* om,
-               cudaStream_t s) {
+               const float* omn, cudaStream_t s) {
   const int B = h->B, P = h->P, M = h->M;
   const int nt = ntiles(P);
   Level& l0 = h->lv[0];
   CK(cudaMemsetAsync(h->z64, 0, sizeof(double) * (size_t)B * M * P, s));
-  PROF(2, s, launch_residual64(l0.G, B, l0.c, rhs, b, om, nullptr, h->rfull, h->part, nullptr, s));
+  PROF(2, s, launch_residual64(l0.G, B, l0.c, rhs, b, om, omn, nullptr, h->rfull, h->part, nullptr, s));
   PROF(7, s, launch_scalar(SC_RHSNORM, B, h->st, h->part, nt, 0.f, 0, s));
   CKL();
   for (int pass = 0; pass < h->opts.max_refine; ++pass) {
@@ -989,7 +1036,7 @@ int solve_core(mpde_hierarchy* h, const float* rhs, const float* b, const float*
     PROF(4, s, launch_backsub(l0.G, B, l0.c, h->rfull, h->x, h->z64, h->st.act, f64_outer(h),
                               h->part, s));
     PROF(7, s, launch_scalar(SC_CORR, B, h->st, h->part, nt, 0.f, 0, s));
-    PROF(2, s, launch_residual64(l0.G, B, l0.c, rhs, b, om, h->z64, h->rfull, h->part, h->st.act, s));
+    PROF(2, s, launch_residual64(l0.G, B, l0.c, rhs, b, om, omn, h->z64, h->rfull, h->part, h->st.act, s));
     PROF(7, s, launch_scalar(SC_REFRES, B, h->st, h->part, nt, 0.f, 0, s));
     CKL();
   }
@@ -1006,7 +1053,7 @@ extern "C" {
 mpde_options mpde_default_options(void) {
   mpde_options o;
   o.tol = 1e-10f;
-  o.tol_z = 1e-4f;
+  o.tol_z = 1e-5f;  // 10x below the north_star z tolerance (Q14: stop margin)
   o.tol_inner = 3e-4f;
   o.max_iters = 500;
   o.max_refine = 6;
@@ -1037,12 +1084,17 @@ int mpde_sizes(const mpde_problem* prob, const mpde_options* opts, int64_t* n_v,
   const int D = prob->ndim;
   int64_t P = 1;
   for (int d = 0; d < D; ++d) P *= prob->n[d];
-  int64_t interior = 1;
-  for (int d = 0; d < D; ++d) interior *= (prob->n[d] - 2);
+  // points on no Dirichlet face, and the Neumann rows (one per point of every Neumann face)
+  int64_t off_dir = 1, neumann = 0;
+  for (int d = 0; d < D; ++d) {
+    off_dir *= prob->n[d] - (prob->bc[d][0] == MPDE_BC_DIRICHLET) - (prob->bc[d][1] == MPDE_BC_DIRICHLET);
+    for (int sd = 0; sd < 2; ++sd)
+      if (prob->bc[d][sd] == MPDE_BC_NEUMANN) neumann += P / prob->n[d];
+  }
   int64_t smooth = 0;
   for (int d = 0; d < D; ++d) smooth += 2 * (int64_t)(prob->n[d] - 1) * (P / prob->n[d]);
   if (n_v) *n_v = (1 + 2 * D) * P;
-  if (n_c) *n_c = P + (P - interior) + 2 * D * P + smooth;
+  if (n_c) *n_c = P + (P - off_dir) + neumann + 2 * D * P + smooth;
   LevelShape shp[kMaxLevels];
   if (n_levels) *n_levels = plan_levels(prob, opts, shp);
   return MPDE_OK;
@@ -1121,7 +1173,8 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
     // per-axis row tables of S (host, fp64 -> fp32) and per-point coefficients
     lv.tab_host.clear();
     for (int d = 0; d < h->prob.ndim; ++d) {
-      const std::vector<float>& t = axis_tables_cached(lv.G.n[d], lv.G.hd[d], lv.G.wr, lv.G.ws);
+      const std::vector<float>& t = axis_tables_cached(lv.G.n[d], lv.G.hd[d], lv.G.wr, lv.G.ws,
+                                                       lv.G.nb2[d][0], lv.G.nb2[d][1]);
       lv.tab_host.insert(lv.tab_host.end(), t.begin(), t.end());
     }
     CK(cudaMemcpyAsync(lv.tab, lv.tab_host.data(), sizeof(float) * lv.tab_host.size(),
@@ -1164,7 +1217,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
         delete h;
         return rc;
       }
-      launch_scalar(SC_LZ_ALPHA, B, sl, h->part, schur_tiles(lv.G, f64_vcycle(h)), 0.f, j, s);
+      launch_scalar(SC_LZ_ALPHA, B, sl, h->part, schur_tiles(lv.G, f64_vcycle(h), B), 0.f, j, s);
       launch_lz_update(lv.P, B, y, v, vp, lv.dinv, h->st.alpha, h->st.beta, h->part, s);
       launch_scalar(SC_LZ_BETA, B, sl, h->part, nt, 0.f, j, s);
       launch_scale(lv.P, B, h->st.alpha, vp, vp, h->ones, s);
@@ -1206,12 +1259,12 @@ int mpde_destroy_hierarchy(mpde_hierarchy* h) {
   return MPDE_OK;
 }
 
-int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, float* z,
-                   mpde_stats* stats, mpde_stream_t stream_) {
+int mpde_solve_fwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* bnd, const float* bnd_n,
+                      float* z, mpde_stats* stats, mpde_stream_t stream_) {
   cudaStream_t s = (cudaStream_t)stream_;
   if (!h || !rhs_b || !bnd || !z) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
   const int B = h->B;
-  if (int rc = solve_core(h, nullptr, rhs_b, bnd, s)) return rc;
+  if (int rc = solve_core(h, nullptr, rhs_b, bnd, bnd_n, s)) return rc;
   PROF(10, s, launch_fwd_out(h->lv[0].G, B, h->lv[0].c, rhs_b, h->z64, z, h->rho, s));
   h->rho_b = rhs_b;
   h->rho_z = z;
@@ -1221,24 +1274,36 @@ int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, floa
   return MPDE_OK;
 }
 
-int mpde_solve_bwd(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,
-                   float* grad_coeff, float* grad_rhs, float* grad_bnd, float* dz_opt,
+int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, float* z,
                    mpde_stats* stats, mpde_stream_t stream_) {
+  return mpde_solve_fwd_bc(h, rhs_b, bnd, nullptr, z, stats, stream_);
+}
+
+int mpde_solve_bwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,
+                      float* grad_coeff, float* grad_rhs, float* grad_bnd, float* grad_bnd_n,
+                      float* dz_opt, mpde_stats* stats, mpde_stream_t stream_) {
   cudaStream_t s = (cudaStream_t)stream_;
   if (!h || !rhs_b || !z || !g_z || !grad_coeff || !grad_rhs || !grad_bnd)
     return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
   const int B = h->B;
   Level& l0 = h->lv[0];
-  if (int rc = solve_core(h, g_z, nullptr, nullptr, s)) return rc;
+  if (int rc = solve_core(h, g_z, nullptr, nullptr, nullptr, s)) return rc;
   // rho kept by the last forward on this handle is used only for the same (rhs_b, z) pair;
   // any other pair (or no forward yet) forms b - c.z from the fp32 z instead
   const bool rho_ok = h->rho_gen != 0 && h->rho_gen == h->fwd_gen && h->rho_b == rhs_b &&
                       h->rho_z == z;
   PROF(10, s, launch_grad(l0.G, B, l0.c, rhs_b, z, rho_ok ? h->rho : nullptr, h->z64,
-                          grad_coeff, grad_rhs, grad_bnd, dz_opt, s));
+                          grad_coeff, grad_rhs, grad_bnd, grad_bnd_n, dz_opt, s));
   if (stats) launch_stats_out(B, h->st, stats, s);
   CKL();
   return MPDE_OK;
+}
+
+int mpde_solve_bwd(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,
+                   float* grad_coeff, float* grad_rhs, float* grad_bnd, float* dz_opt,
+                   mpde_stats* stats, mpde_stream_t stream_) {
+  return mpde_solve_bwd_bc(h, rhs_b, z, g_z, grad_coeff, grad_rhs, grad_bnd, nullptr, dz_opt, stats,
+                           stream_);
 }
 
 int mpde_apply_normal(const mpde_problem* prob, const float* coeff, const float* z, float* q,
@@ -1291,7 +1356,7 @@ int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* d
     }
     case 5: {  // host int32[4]: kernel variants applying S on this level (schur.cu codes)
       int32_t v[4];
-      schur_variants(lv.G, f64_pcg(h), lv.cf16 != nullptr, v);
+      schur_variants(lv.G, f64_pcg(h), lv.cf16 != nullptr, h->B, v);
       std::memcpy(dst, v, sizeof(v));
       return MPDE_OK;
     }
@@ -1316,8 +1381,8 @@ int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* d
 uint64_t mpde_launch_count(void) { return g_launch_count.load(); }
 
 int mpde_profile_begin(void) {
-  if (!g_prof.d_pts) CK(cudaMalloc(&g_prof.d_pts, 16 * sizeof(unsigned long long)));
-  CK(cudaMemset(g_prof.d_pts, 0, 16 * sizeof(unsigned long long)));
+  if (!g_prof.d_pts) CK(cudaMalloc(&g_prof.d_pts, 32 * sizeof(unsigned long long)));
+  CK(cudaMemset(g_prof.d_pts, 0, 32 * sizeof(unsigned long long)));
   g_prof.used = 0;
   g_prof.cls.clear();
   g_prof.on = true;
@@ -1340,9 +1405,9 @@ int mpde_profile_end(double* ms, int64_t* launches, uint64_t* pts) {
     if (launches) launches[c] += 1;
   }
   if (pts) {
-    unsigned long long h[16];
+    unsigned long long h[32];
     CK(cudaMemcpy(h, g_prof.d_pts, sizeof(h), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 16; ++i) pts[i] = h[i];
+    for (int i = 0; i < 32; ++i) pts[i] = h[i];
   }
   return MPDE_OK;
 }

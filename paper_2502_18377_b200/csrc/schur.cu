@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(kThreads) k_schur_coef(Geo G, const float* __r
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     double t11, t12, t22;
-    tinv<double>(G.hd[d], G.wr, G.ws, idx[d] <= G.n[d] - 2, idx[d] >= 1, t11, t12, t22);
+    tinv<double>(G.hd[d], G.wr, G.ws, idx[d] <= G.n[d] - 2, idx[d] >= 1, t11, t12, t22,
+                 double(neu_w2(G, d, idx[d])));
     const double g1 = we * cb[(1 + 2 * d) * P + p], g2 = we * cb[(2 + 2 * d) * P + p];
     u[2 * d] = t11 * g1 + t12 * g2;
     u[2 * d + 1] = t12 * g1 + t22 * g2;
@@ -435,13 +436,13 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const CF* __restrict__ cb
     // boundary rows: faces of the non-last axes cover all 4 points; last-axis faces per point
     bool face = false;
 #pragma unroll
-    for (int d = 0; d < D - 1; ++d) face |= (idx[d] == 0) | (idx[d] == G.n[d] - 1);
+    for (int d = 0; d < D - 1; ++d) face |= dir_face(G, d, idx[d]);
     const float4 x0 = ld4(xb + p0);
     const T wb2 = T(G.wb) * T(G.wb);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int i = idx[D - 1] + j;
-      if (face || i == 0 || i == G.n[D - 1] - 1) acc[j] += wb2 * T(F4(x0, j));
+      if (face || dir_face(G, D - 1, i)) acc[j] += wb2 * T(F4(x0, j));
     }
   }
 #pragma unroll
@@ -832,12 +833,12 @@ __device__ __forceinline__ void quad_y_own(const Geo& G, const CF* __restrict__ 
   const int P = G.P, n = dim_n<NX, NY>(G, 2), i0 = p0 % n;
   {
     const float4 h0 = ld4(hb + p0), c0 = ldc4(cb + p0), x0 = ld4(xb + p0);
-    const bool face = (t == 0) | (t == G.n[0] - 1) | (xr == 0) | (xr == dim_n<NX, NY>(G, 1) - 1);
+    const bool face = dir_face(G, 0, t) | dir_face(G, 1, xr);
     const float wb2 = G.wb * G.wb;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       acc[j] += F4(c0, j) * F4(h0, j);
-      if (face || i0 + j == 0 || i0 + j == n - 1) acc[j] += wb2 * F4(x0, j);
+      if (face || dir_face(G, 2, i0 + j)) acc[j] += wb2 * F4(x0, j);
     }
   }
   const CF* u1 = cb + (size_t)6 * P;
@@ -1352,11 +1353,11 @@ __global__ void k_schur_fused(Geo G, const float* __restrict__ cf, int crep,
               }
             }
           }
-          const bool face = (j == 0) | (j == n0 - 1) | (xo == 0) | (xo == n1 - 1);
+          const bool face = dir_face(G, 0, j) | dir_face(G, 1, xo);
           const float4 x0 = lds4(xr + y0);
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj)
-            if (face || y0 + jj == 0 || y0 + jj == n2 - 1) ay[jj] += wb2 * F4(x0, jj);
+            if (face || dir_face(G, 2, y0 + jj)) ay[jj] += wb2 * F4(x0, jj);
           acc.x += ay[0];
           acc.y += ay[1];
           acc.z += ay[2];
@@ -1610,13 +1611,13 @@ __global__ void __launch_bounds__(4 * NY) k_schur_s_tile(Geo G, const float* __r
         }
       }
       const float4 sa = lds4(SA + (tt * kTX + xx) * NY + y0);
-      const bool face = (t == 0) | (t == n0 - 1) | (xo == 0) | (xo == n1 - 1);
+      const bool face = dir_face(G, 0, t) | dir_face(G, 1, xo);
       const float wb2 = G.wb * G.wb;
       const float sav[4] = {sa.x, sa.y, sa.z, sa.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         acc[j] += sav[j] * hw[4 + j];
-        if (face || y0 + j == 0 || y0 + j == NY - 1) acc[j] += wb2 * xw[8 + j];
+        if (face || dir_face(G, 2, y0 + j)) acc[j] += wb2 * xw[8 + j];
       }
     }
     dot = quad_epilogue<EPI>(A, pde, (size_t)v * P + (size_t)t * s0 + (size_t)xo * NY + y0, x, acc);
@@ -1702,14 +1703,13 @@ __global__ void __launch_bounds__(kThreads) k_schur_hy(Geo G, const float* __res
     bw[4 * k] = vb.x; bw[4 * k + 1] = vb.y; bw[4 * k + 2] = vb.z; bw[4 * k + 3] = vb.w;
   }
   float ry[4];
-  const bool face = (idx[0] == 0) | (idx[0] == G.n[0] - 1) | (idx[1] == 0) |
-                    (idx[1] == dim_n<NX, NY>(G, 1) - 1);
+  const bool face = dir_face(G, 0, idx[0]) | dir_face(G, 1, idx[1]);
   const float wb2 = G.wb * G.wb;
   const float sav[4] = {csa.x, csa.y, csa.z, csa.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     float a = sav[j] * hq[j];
-    if (face || y0 + j == 0 || y0 + j == nl - 1) a += wb2 * xw[8 + j];
+    if (face || dir_face(G, 2, y0 + j)) a += wb2 * xw[8 + j];
     if (ymode == 1) {
 #pragma unroll
       for (int o = -4; o <= 4; ++o) a += G.irow[2][20 + o + 4] * xw[8 + j + o];
@@ -1849,7 +1849,8 @@ static inline bool use_tile(const Geo& G, bool f64) {
   return (n2 == 32 || n2 == 64 || n2 == 128) && G.n[1] % kTX == 0 && G.n[1] >= 2 * kTX;
 }
 static inline int tile_ctas(const Geo& G) { return ((G.n[0] + kTT - 1) / kTT) * (G.n[1] / kTX); }
-int schur_tiles(const Geo& G, bool f64) {
+// CTAs per vector of the two-pass pass-2 kernel (grid x of its launches)
+static int schur_tiles2p(const Geo& G, bool f64) {
   if (use_fused(G, f64)) return G.n[1] / kFX;
   if (use_tile(G, f64)) return tile_ctas(G);
   if (use_b22(G, f64)) return b22_ctas(G);
@@ -1858,6 +1859,10 @@ int schur_tiles(const Geo& G, bool f64) {
     return (G.P + 4 * th - 1) / (4 * th);
   }
   return (G.P + kThreads - 1) / kThreads;
+}
+
+int schur_tiles(const Geo& G, bool f64, int nvec) {
+  return use_march(G, f64, nvec) ? march_ctas(G) : schur_tiles2p(G, f64);
 }
 
 void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const float* x, void* g,
@@ -1926,7 +1931,7 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
     return;
   }
   if (use_b22(G, f64)) {
-    const dim3 gb(schur_tiles(G, f64), nvec);
+    const dim3 gb(schur_tiles2p(G, f64), nvec);
     const int rm = use_remap(G) ? b22_tp(G) : 0;  // >1: t-pair tiling (remap implied)
 #define B22_LAUNCH(E, BXv, YPv)                                                              \
   if (G.n[1] == 64 && G.n[2] == 64)                                                          \
@@ -1963,7 +1968,7 @@ void launch_schur_out(int epi, const Geo& G, int nvec, int crep, const float* cf
   const bool v4 = use_v4(G);
   const int rm = use_remap(G);
   const int th = v4 ? v4_threads(G) : kThreads;
-  dim3 gr(schur_tiles(G, f64), nvec);
+  dim3 gr(schur_tiles2p(G, f64), nvec);
 #define EPI_CASE2(E)                                                                              \
   case E:                                                                                         \
     if (v4) {                                                                                     \
@@ -2009,7 +2014,7 @@ void launch_schur_out_bf(int epi, const Geo& G, int nvec, int crep, const void* 
   const __nv_bfloat16* cf = static_cast<const __nv_bfloat16*>(cf16);
   const float* gf = static_cast<const float*>(g);
   if (use_b22(G, false)) {
-    const dim3 gb(schur_tiles(G, false), nvec);
+    const dim3 gb(schur_tiles2p(G, false), nvec);
     const int rm = use_remap(G) ? b22_tp(G) : 0;
 #define B22BF(E)                                                                                  \
   case E:                                                                                         \
@@ -2033,7 +2038,7 @@ void launch_schur_out_bf(int epi, const Geo& G, int nvec, int crep, const void* 
   }
   const int rm = use_remap(G);
   const int th = v4_threads(G);
-  dim3 gr(schur_tiles(G, false), nvec);
+  dim3 gr(schur_tiles2p(G, false), nvec);
 #define V4BF(E)                                                                                   \
   case E:                                                                                         \
     DISPATCH_D2(G.D, (k_schur_s_v4<DD, E, float, __nv_bfloat16><<<gr, th, 0, s>>>(G, cf, crep, x, gf, A, act, rm))); \
@@ -2080,7 +2085,8 @@ void launch_schur_fused(int epi, const Geo& G, int nvec, int crep, const float* 
 //   out[0] pass 1 of the PCG operator, out[1] pass 2 of the PCG operator,
 //   out[2] pass 2 of the V-cycle applies, out[3] 1 if those read bf16 coefficients.
 // Codes: 0 scalar, 1 v4, 2 v4 warp-specialised, 3 t-blocked (runtime extents),
-// 4 t-blocked (compile-time extents), 5 2x2-blocked, 6 smem tile, 7 fused, 8 pass 1 with y part.
+// 4 t-blocked (compile-time extents), 5 2x2-blocked, 6 smem tile, 7 fused, 8 pass 1 with y part,
+// 9 one-kernel t-marching apply (march.cu).
 static int pass2_kind(const Geo& G, bool f64) {
   if (use_fused(G, f64)) return 7;
   if (use_tile(G, f64)) return 6;
@@ -2092,7 +2098,12 @@ static int pass2_kind(const Geo& G, bool f64) {
   if (use_v4(G)) return use_remap(G) ? 2 : 1;
   return 0;
 }
-void schur_variants(const Geo& G, bool f64, bool bf16_level, int32_t out[4]) {
+void schur_variants(const Geo& G, bool f64, bool bf16_level, int nvec, int32_t out[4]) {
+  if (use_march(G, f64, nvec)) {  // one kernel for every apply; V-cycle applies read bf16 cf if kept
+    out[0] = out[1] = out[2] = 9;
+    out[3] = bf16_level ? 1 : 0;
+    return;
+  }
   out[0] = use_fused(G, f64) ? 7 : use_hy(G, f64) ? 8 : use_v4(G) ? 1 : 0;
   out[1] = pass2_kind(G, f64);
   const bool bf = bf16_level && schur_bf16_ok(G, f64);

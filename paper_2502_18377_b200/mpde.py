@@ -23,7 +23,11 @@ LIB_PATH = os.path.join(_HERE, "libmpde.so")
 class mpde_problem(C.Structure):
     _fields_ = [("ndim", C.c_int32), ("n", C.c_int32 * 4), ("h", C.c_double * 4),
                 ("batch", C.c_int32), ("deriv_order", C.c_int32), ("w_eq", C.c_float),
-                ("w_bnd", C.c_float), ("w_deriv", C.c_float), ("w_smooth", C.c_float)]
+                ("w_bnd", C.c_float), ("w_deriv", C.c_float), ("w_smooth", C.c_float),
+                ("bc", (C.c_int32 * 2) * 4)]
+
+
+BC_CODES = {"D": 0, "N": 1, "-": 2, 0: 0, 1: 1, 2: 2}
 
 
 class mpde_options(C.Structure):
@@ -67,6 +71,8 @@ def lib():
         L.mpde_build_hierarchy.argtypes = [P, O, vp, vp, C.c_size_t, S, C.POINTER(vp)]
         L.mpde_solve_fwd.argtypes = [vp, vp, vp, vp, vp, S]
         L.mpde_solve_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, S]
+        L.mpde_solve_fwd_bc.argtypes = [vp, vp, vp, vp, vp, vp, S]
+        L.mpde_solve_bwd_bc.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, S]
         L.mpde_destroy_hierarchy.argtypes = [vp]
         L.mpde_apply_normal.argtypes = [P, vp, vp, vp, S]
         L.mpde_apply_schur.argtypes = [vp, C.c_int32, vp, vp, S]
@@ -91,13 +97,14 @@ def lib():
 
 
 EXPORTS = ["mpde_default_options", "mpde_sizes", "mpde_workspace_bytes", "mpde_build_hierarchy",
-           "mpde_solve_fwd", "mpde_solve_bwd", "mpde_destroy_hierarchy", "mpde_last_error",
+           "mpde_solve_fwd", "mpde_solve_bwd", "mpde_solve_fwd_bc", "mpde_solve_bwd_bc", "mpde_destroy_hierarchy", "mpde_last_error",
            "mpde_apply_normal", "mpde_apply_schur", "mpde_apply_precond", "mpde_hierarchy_query",
            "mpde_host_staging_bytes", "mpde_fwd_bwd_host", "mpde_batch_sum",
            "mpde_profile_begin", "mpde_profile_end", "mpde_launch_count", "mpde_template_terms",
            "mpde_template_coeff", "mpde_template_workspace_bytes", "mpde_template_grad"]
 PROF_CLASSES = ["schur_g", "schur_out", "residual64", "condense", "backsub", "transfer",
-                "vector", "scalar", "coarse", "build", "epilogue", "schur_out_l0", "schur_g_l0"]
+                "vector", "scalar", "coarse", "build", "epilogue", "schur_out_l0", "schur_g_l0",
+                "schur_march_l0", "schur_march"]
 
 
 def _check(rc):
@@ -105,7 +112,9 @@ def _check(rc):
         raise RuntimeError(f"mpde error {rc}: {lib().mpde_last_error().decode()}")
 
 
-def make_problem(shape, h, batch, w_eq=1.0, w_bnd=1.0, w_deriv=1.0, w_smooth=1.0):
+def make_problem(shape, h, batch, w_eq=1.0, w_bnd=1.0, w_deriv=1.0, w_smooth=1.0, bc=None):
+    """bc: per dim (low, high) face types, 'D' Dirichlet / 'N' Neumann / '-' none (or the
+    MPDE_BC_* codes); None = every face Dirichlet."""
     pr = mpde_problem()
     pr.ndim = len(shape)
     for d, (n, hh) in enumerate(zip(shape, h)):
@@ -114,6 +123,9 @@ def make_problem(shape, h, batch, w_eq=1.0, w_bnd=1.0, w_deriv=1.0, w_smooth=1.0
     pr.batch = int(batch)
     pr.deriv_order = 2
     pr.w_eq, pr.w_bnd, pr.w_deriv, pr.w_smooth = w_eq, w_bnd, w_deriv, w_smooth
+    if bc is not None:
+        for d, (lo, hi) in enumerate(bc):
+            pr.bc[d][0], pr.bc[d][1] = BC_CODES[lo], BC_CODES[hi]
     return pr
 
 
@@ -173,6 +185,19 @@ def mpde_solve_bwd(h, rhs_b, z, g_z, grad_coeff, grad_rhs, grad_bnd, dz=None, st
                                 _ptr(stats), _stream(stream)))
 
 
+def mpde_solve_fwd_bc(h, rhs_b, bnd, bnd_n, z, stats=None, stream=None):
+    _check(lib().mpde_solve_fwd_bc(h, _ptr(_dev_f32(rhs_b, "rhs_b")), _ptr(_dev_f32(bnd, "bnd")),
+                                   None if bnd_n is None else _ptr(_dev_f32(bnd_n, "bnd_n")),
+                                   _ptr(_dev_f32(z, "z")), _ptr(stats), _stream(stream)))
+
+
+def mpde_solve_bwd_bc(h, rhs_b, z, g_z, grad_coeff, grad_rhs, grad_bnd, grad_bnd_n, dz=None,
+                      stats=None, stream=None):
+    _check(lib().mpde_solve_bwd_bc(h, _ptr(rhs_b), _ptr(z), _ptr(_dev_f32(g_z, "g_z")),
+                                   _ptr(grad_coeff), _ptr(grad_rhs), _ptr(grad_bnd),
+                                   _ptr(grad_bnd_n), _ptr(dz), _ptr(stats), _stream(stream)))
+
+
 def mpde_destroy_hierarchy(h):
     _check(lib().mpde_destroy_hierarchy(h))
 
@@ -192,7 +217,7 @@ def mpde_apply_precond(h, r, z, stream=None):
 def mpde_hierarchy_query(h, level, what, dst, stream=None):
     if what in (0, 5):
         arr = (C.c_int32 * 4)()
-        _check(lib().mpde_hierarchy_query(h, int(level), 0, C.cast(arr, C.c_void_p),
+        _check(lib().mpde_hierarchy_query(h, int(level), int(what), C.cast(arr, C.c_void_p),
                                           _stream(stream)))
         return list(arr)
     _check(lib().mpde_hierarchy_query(h, int(level), int(what), _ptr(dst), _stream(stream)))
@@ -214,11 +239,11 @@ def mpde_profile_begin():
 
 
 def mpde_profile_end():
-    """-> (dict class -> (ms, launches), pts[16])"""
+    """-> (dict class -> (ms, launches), pts[32])"""
     n = len(PROF_CLASSES)
     ms = (C.c_double * n)()
     cnt = (C.c_int64 * n)()
-    pts = (C.c_uint64 * 16)()
+    pts = (C.c_uint64 * 32)()
     _check(lib().mpde_profile_end(C.cast(ms, C.c_void_p), C.cast(cnt, C.c_void_p),
                                   C.cast(pts, C.c_void_p)))
     return {k: (ms[i], cnt[i]) for i, k in enumerate(PROF_CLASSES)}, list(pts)
@@ -278,12 +303,13 @@ class Solver:
     follow mpde.h; stats are returned as a list of dicts after a stream sync.
     """
 
-    def __init__(self, shape, h, c, opts=None, weights=(1.0, 1.0, 1.0, 1.0), stream=None):
+    def __init__(self, shape, h, c, opts=None, weights=(1.0, 1.0, 1.0, 1.0), stream=None, bc=None):
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required (no CPU fallback)")
         self.shape, self.h = tuple(shape), tuple(h)
         self.B, self.M, self.P = c.shape
-        self.prob = make_problem(shape, h, self.B, *weights)
+        self.prob = make_problem(shape, h, self.B, *weights, bc=bc)
+        self.D = len(self.shape)
         self.opts = opts if opts is not None else mpde_default_options()
         self.c = _dev_f32(c, "c")
         nbytes = mpde_workspace_bytes(self.prob, self.opts)
@@ -291,17 +317,24 @@ class Solver:
         self.stats = torch.zeros((self.B, 5), dtype=torch.int32, device=c.device)
         self.h_ = mpde_build_hierarchy(self.prob, self.opts, self.c, self.ws, stream)
 
-    def forward(self, b, omega, stream=None):
+    def forward(self, b, omega, stream=None, omega_n=None):
+        """omega_n: [B][D][P] Neumann data (faces of type 'N'); None = 0."""
         z = torch.empty((self.B, self.M, self.P), dtype=torch.float32, device=self.c.device)
-        mpde_solve_fwd(self.h_, b, omega, z, self.stats, stream)
+        mpde_solve_fwd_bc(self.h_, b, omega, omega_n, z, self.stats, stream)
         return z
 
-    def backward(self, b, z, g, want_dz=False, stream=None):
+    def backward(self, b, z, g, want_dz=False, stream=None, want_grad_omega_n=False):
+        """-> (grad_c, grad_b, grad_omega, dz) or, with want_grad_omega_n, the same plus
+        dl/domega_n [B][D][P]."""
         gc = torch.empty_like(self.c)
         gb = torch.empty((self.B, self.P), dtype=torch.float32, device=self.c.device)
         gw = torch.empty_like(gb)
         dz = torch.empty_like(self.c) if want_dz else None
-        mpde_solve_bwd(self.h_, b, z, g, gc, gb, gw, dz, self.stats, stream)
+        gwn = (torch.empty((self.B, self.D, self.P), dtype=torch.float32, device=self.c.device)
+               if want_grad_omega_n else None)
+        mpde_solve_bwd_bc(self.h_, b, z, g, gc, gb, gw, gwn, dz, self.stats, stream)
+        if want_grad_omega_n:
+            return gc, gb, gw, dz, gwn
         return gc, gb, gw, dz
 
     def stats_list(self):

@@ -73,23 +73,33 @@ np.save(sys.argv[3], np.array(mpde.mpde_hierarchy_query(s.h_, 0, 5, None)))
 # levels above MPDE_SMALLP = 16384 points per vector select the production kernels; below it
 # the 64-thread v4 kernels run whatever the switches say, so the variant cases set
 # MPDE_SMALLP=0 and every case asserts the kernel that actually ran.
-_NOSMALL = {"MPDE_SMALLP": "0"}
-@pytest.mark.parametrize("shape,h,env,kinds", [
-    ((6, 64, 64), (0.01, 1 / 64, 1 / 64), {}, (1, 4)),        # C4 level-0 kernel <64,64> (production)
-    ((20, 32, 32), (0.02, 1 / 32, 1 / 32), {}, (1, 4)),       # C4 level-1 kernel <32,32> (production)
-    ((6, 128, 128), (0.005, 1 / 128, 1 / 128), {}, (1, 4)),   # C5 level-0 kernel <128,128>
-    ((17, 24, 48), (0.05, 0.06, 0.07), {}, (1, 3)),           # runtime extents (NY4 = 12, no remap)
-    ((7, 16, 32), (0.05, 0.06, 0.07), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7)),  # fused, 2 x-tiles
-    ((9, 24, 36), (0.04, 0.03, 0.05), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7)),  # fused, interior tile
-    ((7, 16, 64), (0.05, 0.06, 0.07), _NOSMALL, (1, 3)),      # t-blocked, warp-specialised y (NY4=16)
-    ((8, 10, 32), (0.05, 0.06, 0.07), _NOSMALL, (1, 3)),      # t-blocked, NY4=8 (4 interior / 4 edge)
-    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_HY": "1", **_NOSMALL}, (8, 3)),  # y part in pass 1
-    ((9, 12, 32), (0.05, 0.06, 0.07), {"MPDE_HY": "1", **_NOSMALL}, (8, 3)),
-    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_TILE": "1", **_NOSMALL}, (1, 6)),   # smem-tiled pass 2
-    ((13, 12, 32), (0.05, 0.06, 0.07), {"MPDE_TILE": "1", **_NOSMALL}, (1, 6)),  # partial last t tile
-    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_B22_TP": "4", **_NOSMALL}, (1, 3)),  # t-pair CTA tiling
-    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_SCHUR_BLOCK": "2", **_NOSMALL}, (1, 5))])  # 2x2 blocking
-def test_large_schur_matches_sparse(shape, h, env, kinds, tmp_path):
+_NOSMALL = {"MPDE_SMALLP": "0", "MPDE_MARCH": "0"}
+_NOMARCH = {"MPDE_MARCH": "0"}
+_MARCH = {"MPDE_MARCH": "2"}  # the march on every eligible level, whatever the grid size
+@pytest.mark.parametrize("shape,h,env,kinds,B", [
+    # production: the one-kernel t-marching apply (code 9, march.cu) on launches with >= 148 CTAs
+    ((6, 64, 64), (0.01, 1 / 64, 1 / 64), {}, (9, 9), 19),     # C4 level-0 geometry, 152 CTAs
+    ((20, 32, 32), (0.02, 1 / 32, 1 / 32), {}, (1, 4), 2),      # small launch: two-pass <32,32>
+    ((20, 32, 32), (0.02, 1 / 32, 1 / 32), _MARCH, (9, 9), 2),  # NY 32, 4 strips
+    ((7, 16, 64), (0.05, 0.06, 0.07), _MARCH, (9, 9), 2),       # 2 strips, both edge strips
+    ((9, 24, 32), (0.05, 0.06, 0.07), _MARCH, (9, 9), 2),       # 3 strips, one interior strip
+    ((11, 40, 64), (0.03, 0.04, 0.02), _MARCH, (9, 9), 2),      # 5 strips, t extent 11
+    ((8, 64, 128), (0.02, 0.03, 0.01), _MARCH, (9, 9), 2),      # NY 128 (512-thread CTAs)
+    # the two-pass kernels the march replaces (and where it does not apply)
+    ((6, 64, 64), (0.01, 1 / 64, 1 / 64), _NOMARCH, (1, 4), 2), # t-blocked pass 2 <64,64>
+    ((6, 128, 128), (0.005, 1 / 128, 1 / 128), {}, (1, 4), 2),  # C5 level 0: 16 strips > 8, <128,128>
+    ((17, 24, 48), (0.05, 0.06, 0.07), {}, (1, 3), 2),          # runtime extents (NY4 = 12, no remap)
+    ((7, 16, 32), (0.05, 0.06, 0.07), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7), 2),  # fused, 2 x-tiles
+    ((9, 24, 36), (0.04, 0.03, 0.05), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7), 2),  # fused, interior tile
+    ((7, 16, 64), (0.05, 0.06, 0.07), _NOSMALL, (1, 3), 2),      # t-blocked, warp-specialised y (NY4=16)
+    ((8, 10, 32), (0.05, 0.06, 0.07), _NOSMALL, (1, 3), 2),      # t-blocked, NY4=8 (4 interior / 4 edge)
+    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_HY": "1", **_NOSMALL}, (8, 3), 2),  # y part in pass 1
+    ((9, 12, 32), (0.05, 0.06, 0.07), {"MPDE_HY": "1", **_NOSMALL}, (8, 3), 2),
+    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_TILE": "1", **_NOSMALL}, (1, 6), 2),   # smem-tiled pass 2
+    ((13, 12, 32), (0.05, 0.06, 0.07), {"MPDE_TILE": "1", **_NOSMALL}, (1, 6), 2),  # partial last t tile
+    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_B22_TP": "4", **_NOSMALL}, (1, 3), 2),  # t-pair CTA tiling
+    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_SCHUR_BLOCK": "2", **_NOSMALL}, (1, 5), 2)])  # 2x2 blocking
+def test_large_schur_matches_sparse(shape, h, env, kinds, B, tmp_path):
     """S apply through every 3D kernel variant, incl. the production instantiations the
     bench runs (the selection switches are read once per process, so the apply runs in a child
     process), against S applied through the oracle's sparse A (no dense N at these sizes)."""
@@ -97,7 +107,7 @@ def test_large_schur_matches_sparse(shape, h, env, kinds, tmp_path):
     import subprocess
     import sys
     rng = np.random.default_rng(7)
-    M, P, B = 7, int(np.prod(shape)), 2
+    M, P = 7, int(np.prod(shape))
     c = rng.normal(0.0, 0.5, (B, M, P))
     c[:, 1] += 1.0
     c = c.astype(np.float32)
@@ -112,29 +122,31 @@ def test_large_schur_matches_sparse(shape, h, env, kinds, tmp_path):
     v = np.load(tmp_path / "v.npy")
     assert (int(v[0]), int(v[1])) == kinds, f"kernel variants {v.tolist()} != expected {kinds}"
     pr = Problem(shape, h, *w)
-    for i in range(B):
+    for i in sorted({0, 1, B - 1}):  # first, second and last PDE of the launch
         ref = _sparse_schur_apply(pr, c[i].astype(np.float64), x[i].astype(np.float64))
         assert np.linalg.norm(y[i] - ref) <= 1e-4 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("shape,h", [((16, 18, 20), (0.05, 0.06, 0.07)), ((20, 24), (0.05, 0.04)),
-                                     ((20, 32, 32), (0.05, 0.03, 0.03)),
-                                     ((6, 64, 64), (0.01, 1 / 64, 1 / 64)),
-                                     ((64, 96), (0.05, 0.02))])
-def test_vcycle_symmetric_positive(shape, h):
+@pytest.mark.parametrize("shape,h,B", [((16, 18, 20), (0.05, 0.06, 0.07), 2), ((20, 24), (0.05, 0.04), 2),
+                                       ((20, 32, 32), (0.05, 0.03, 0.03), 2),
+                                       ((6, 64, 64), (0.01, 1 / 64, 1 / 64), 19),
+                                       ((64, 96), (0.05, 0.02), 2)])
+def test_vcycle_symmetric_positive(shape, h, B):
     """The V-cycle is a fixed SPD linear map (needed by PCG): <Ma, b> = <a, Mb>, <Ma, a> > 0.
-    (20,32,32) and (6,64,64) run the level-0 V-cycle applies through the bf16-coefficient
-    t-blocked kernels <32,32> / <64,64> the bench uses (asserted)."""
+    (20,32,32) runs the level-0 V-cycle applies through the bf16-coefficient t-blocked
+    two-pass kernels, (6,64,64) with 19 PDEs (152 CTAs) through the bf16 t-marching kernel
+    the bench uses (both asserted)."""
     from paper_2502_18377_b200 import mpde
     rng = np.random.default_rng(6)
     D = len(shape)
-    M, P, B = 1 + 2 * D, int(np.prod(shape)), 2
+    M, P = 1 + 2 * D, int(np.prod(shape))
     c = rng.normal(0.0, 0.5, (B, M, P))
     c[:, 1] += 1.0
     s = mpde.Solver(shape, h, torch.from_numpy(c.astype(np.float32)).cuda())
     if P > 16384 and D == 3:
         v = mpde.mpde_hierarchy_query(s.h_, 0, 5, None)
-        assert v[2] == 4 and v[3] == 1, v  # t-blocked <n,n> kernel reading bf16 coefficients
+        want = 9 if B * (shape[1] // 8) >= 148 else 4  # t-marching / t-blocked <n,n>
+        assert v[2] == want and v[3] == 1, v  # reading bf16 coefficients
     a = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()
     b = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()
     ma, mb = torch.empty_like(a), torch.empty_like(b)
