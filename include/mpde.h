@@ -175,9 +175,16 @@ int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, floa
  * bnd_n [B][ndim][P] (device, read only on the Neumann faces of dim d; NULL = homogeneous
  * Neumann data, omega_n = 0); grad_bnd_n [B][ndim][P] (device, written: dl/domega_n on the
  * Neumann faces of dim d, 0 elsewhere; NULL = not computed).  mpde_solve_fwd / _bwd are these
- * calls with NULL Neumann arguments. */
+ * calls with NULL Neumann arguments.
+ * lambda_opt (device, written, or NULL): the duals lambda* = d - A z* (Eq. 10 first block row,
+ * P:200-214), computed in fp64 from the forward's fp64 solution, in a structured
+ * layout [B][2 + 5*ndim][P]: slot 0 the equation row of p (Eq. 3), 1 its Dirichlet row (0 if p
+ * has none), 2 + d the Neumann row of dim d (0 off the Neumann faces of d), 2 + ndim + 2d + (k-1)
+ * the derivative row (d, k) (Eq. 5), 2 + 3 ndim + 2d + {0 forward, 1 backward} the Taylor rows
+ * (Eqs. 6-7; 0 where the neighbour does not exist).  Each slot holds the row's weighted
+ * residual, e.g. w_eq (b - sum_m c_m z_m) for slot 0. */
 int mpde_solve_fwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* bnd, const float* bnd_n,
-                      float* z, mpde_stats* stats, mpde_stream_t stream);
+                      float* z, float* lambda_opt, mpde_stats* stats, mpde_stream_t stream);
 int mpde_solve_bwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,
                       float* grad_coeff, float* grad_rhs, float* grad_bnd, float* grad_bnd_n,
                       float* dz_opt, mpde_stats* stats, mpde_stream_t stream);

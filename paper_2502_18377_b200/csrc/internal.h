@@ -183,6 +183,8 @@ void launch_gm_scalar(int op, int j, int m, int P, int B, const PdeState& st, co
 void launch_count_active(int B, const int* act, int* out, cudaStream_t s);
 void launch_smooth_coef(int B, int nu, int kind, float theta, float ratio, const double* lmax,
                         float* coef, cudaStream_t s);
+void launch_duals(const Geo& G, int B, const float* c, const float* b, const float* om,
+                  const float* omn, const double* z64, float* lam, cudaStream_t s);
 void launch_grad(const Geo& G, int B, const float* c, const float* b, const float* z,
                  const float* rho, const double* dz64, float* gc, float* gb, float* gw,
                  float* gwn, float* dz_out, cudaStream_t s);

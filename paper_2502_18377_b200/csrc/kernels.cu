@@ -995,6 +995,62 @@ __global__ void __launch_bounds__(kThreads) k_fwd_out(Geo G, const float* __rest
   rho[(size_t)v * P + p] = float(r);
 }
 
+// duals lambda* = d - A z* (Eq. 10 first block row, reading Q8), fp64 from the
+// forward's fp64 z, one thread per point writing every row the point owns, structured layout
+// [B][2 + 5D][P]: slot 0 equation row (Eq. 3), 1 Dirichlet row (Eq. 4; 0 where the point has
+// none), 2..2+D-1 Neumann row of dim d, then derivative rows (d, k = 1, 2) (Eq. 5)
+// and smoothness rows (d, forward / backward) (Eqs. 6-7), 0 where a row is absent.
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_duals(Geo G, const float* __restrict__ c,
+                                                   const float* __restrict__ b,
+                                                   const float* __restrict__ om,
+                                                   const float* __restrict__ omn,
+                                                   const double* __restrict__ z64,
+                                                   float* __restrict__ lam) {
+  MPDE_PDL_ENTRY();
+  constexpr int M = 1 + 2 * D, NS = 2 + 5 * D;
+  const int v = blockIdx.y, P = G.P;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int idx[D];
+  unravel<D>(G, p, idx);
+  const double* zb = z64 + (size_t)v * M * P;
+  const float* cb = c + (size_t)v * M * P;
+  float* out = lam + (size_t)v * NS * P + p;
+  double e = double(b[(size_t)v * P + p]);
+#pragma unroll
+  for (int m = 0; m < M; ++m) e -= double(cb[(size_t)m * P + p]) * zb[(size_t)m * P + p];
+  out[0] = float(double(G.we) * e);
+  out[(size_t)P] = on_boundary<D>(G, idx) ? float(double(G.wb) * (double(om[(size_t)v * P + p]) - zb[p])) : 0.f;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const bool neu = neu_w2(G, d, idx[d]) != 0.f;
+    const double dat = (neu && omn) ? double(omn[((size_t)v * D + d) * P + p]) : 0.0;
+    out[(size_t)(2 + d) * P] = neu ? float(double(G.wb) * (dat - zb[(size_t)(1 + 2 * d) * P + p])) : 0.f;
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const int n = G.n[d], s = G.stride[d], i = idx[d];
+    const double h = G.hd[d], h2 = G.h2d[d];
+    const int cls = fd_cls(i, n), st = fd_start(cls);
+    double D1 = 0.0, D2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const double zv = zb[p + (st + q) * s];
+      D1 += cAd[0][cls][q] * zv;
+      D2 += cAd[1][cls][q] * zv;
+    }
+    const double zd1 = zb[(size_t)(1 + 2 * d) * P + p], zd2 = zb[(size_t)(2 + 2 * d) * P + p];
+    out[(size_t)(2 + D + 2 * d) * P] = float(-double(G.wr) * (h * zd1 - D1));
+    out[(size_t)(2 + D + 2 * d + 1) * P] = float(-double(G.wr) * (h2 * zd2 - D2));
+    const double z0 = zb[p];
+    out[(size_t)(2 + 3 * D + 2 * d) * P] =
+        i <= n - 2 ? float(-double(G.ws) * (z0 + h * zd1 + 0.5 * h2 * zd2 - zb[p + s])) : 0.f;
+    out[(size_t)(2 + 3 * D + 2 * d + 1) * P] =
+        i >= 1 ? float(-double(G.ws) * (z0 - h * zd1 + 0.5 * h2 * zd2 - zb[p - s])) : 0.f;
+  }
+}
+
 // out[j] = sum_b x[b][j], fixed summation order (deterministic)
 __global__ void __launch_bounds__(kThreads) k_batch_sum(const float* __restrict__ x, int B,
                                                        int64_t n, float* __restrict__ out) {
@@ -1206,6 +1262,11 @@ void launch_fwd_out(const Geo& G, int B, const float* c, const float* b, const d
                     float* z, float* rho, cudaStream_t s) {
   ++g_launch_count;
   DISPATCH_D(G.D, k_fwd_out<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, b, z64, z, rho));
+}
+void launch_duals(const Geo& G, int B, const float* c, const float* b, const float* om,
+                  const float* omn, const double* z64, float* lam, cudaStream_t s) {
+  ++g_launch_count;
+  DISPATCH_D(G.D, k_duals<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, b, om, omn, z64, lam));
 }
 void launch_batch_sum(const float* x, int B, int64_t n, float* out, cudaStream_t s) {
   ++g_launch_count;

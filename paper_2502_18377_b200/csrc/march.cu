@@ -644,7 +644,8 @@ __global__ void __launch_bounds__(MarchSmem<NY, CF>::THREADS)
   }
 }
 
-int g_march = -1;  // env MPDE_MARCH (default 1): 0 disables the t-marching kernel, 2 forces it
+int g_march = -1;  // env MPDE_MARCH: 0 (default) two-pass kernels, 1 the march on launches with
+                   // >= 148 CTAs, 2 the march on every eligible level (tests)
 }  // namespace
 
 // 3D levels the t-marching kernel handles: NY in {32, 64, 128}, NX a multiple of 8 with
@@ -653,7 +654,7 @@ int g_march = -1;  // env MPDE_MARCH (default 1): 0 disables the t-marching kern
 bool use_march(const Geo& G, bool f64, int nvec) {
   if (g_march < 0) {
     const char* e = getenv("MPDE_MARCH");
-    g_march = e ? atoi(e) : 1;
+    g_march = e ? atoi(e) : 0;  // opt-in: at C4 it ties the two-pass kernels
   }
   if (!g_march || f64 || G.D != 3) return false;
   const int ny = G.n[2], nx = G.n[1];

@@ -1260,12 +1260,14 @@ int mpde_destroy_hierarchy(mpde_hierarchy* h) {
 }
 
 int mpde_solve_fwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* bnd, const float* bnd_n,
-                      float* z, mpde_stats* stats, mpde_stream_t stream_) {
+                      float* z, float* lambda_opt, mpde_stats* stats, mpde_stream_t stream_) {
   cudaStream_t s = (cudaStream_t)stream_;
   if (!h || !rhs_b || !bnd || !z) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
   const int B = h->B;
   if (int rc = solve_core(h, nullptr, rhs_b, bnd, bnd_n, s)) return rc;
   PROF(10, s, launch_fwd_out(h->lv[0].G, B, h->lv[0].c, rhs_b, h->z64, z, h->rho, s));
+  if (lambda_opt)
+    PROF(10, s, launch_duals(h->lv[0].G, B, h->lv[0].c, rhs_b, bnd, bnd_n, h->z64, lambda_opt, s));
   h->rho_b = rhs_b;
   h->rho_z = z;
   h->rho_gen = ++h->fwd_gen;
@@ -1276,7 +1278,7 @@ int mpde_solve_fwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* bnd, c
 
 int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, float* z,
                    mpde_stats* stats, mpde_stream_t stream_) {
-  return mpde_solve_fwd_bc(h, rhs_b, bnd, nullptr, z, stats, stream_);
+  return mpde_solve_fwd_bc(h, rhs_b, bnd, nullptr, z, nullptr, stats, stream_);
 }
 
 int mpde_solve_bwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,

@@ -71,7 +71,7 @@ def lib():
         L.mpde_build_hierarchy.argtypes = [P, O, vp, vp, C.c_size_t, S, C.POINTER(vp)]
         L.mpde_solve_fwd.argtypes = [vp, vp, vp, vp, vp, S]
         L.mpde_solve_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, S]
-        L.mpde_solve_fwd_bc.argtypes = [vp, vp, vp, vp, vp, vp, S]
+        L.mpde_solve_fwd_bc.argtypes = [vp, vp, vp, vp, vp, vp, vp, S]
         L.mpde_solve_bwd_bc.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, S]
         L.mpde_destroy_hierarchy.argtypes = [vp]
         L.mpde_apply_normal.argtypes = [P, vp, vp, vp, S]
@@ -185,10 +185,12 @@ def mpde_solve_bwd(h, rhs_b, z, g_z, grad_coeff, grad_rhs, grad_bnd, dz=None, st
                                 _ptr(stats), _stream(stream)))
 
 
-def mpde_solve_fwd_bc(h, rhs_b, bnd, bnd_n, z, stats=None, stream=None):
+def mpde_solve_fwd_bc(h, rhs_b, bnd, bnd_n, z, stats=None, stream=None, lambda_opt=None):
     _check(lib().mpde_solve_fwd_bc(h, _ptr(_dev_f32(rhs_b, "rhs_b")), _ptr(_dev_f32(bnd, "bnd")),
                                    None if bnd_n is None else _ptr(_dev_f32(bnd_n, "bnd_n")),
-                                   _ptr(_dev_f32(z, "z")), _ptr(stats), _stream(stream)))
+                                   _ptr(_dev_f32(z, "z")),
+                                   None if lambda_opt is None else _ptr(_dev_f32(lambda_opt, "lambda_opt")),
+                                   _ptr(stats), _stream(stream)))
 
 
 def mpde_solve_bwd_bc(h, rhs_b, z, g_z, grad_coeff, grad_rhs, grad_bnd, grad_bnd_n, dz=None,
@@ -317,11 +319,14 @@ class Solver:
         self.stats = torch.zeros((self.B, 5), dtype=torch.int32, device=c.device)
         self.h_ = mpde_build_hierarchy(self.prob, self.opts, self.c, self.ws, stream)
 
-    def forward(self, b, omega, stream=None, omega_n=None):
-        """omega_n: [B][D][P] Neumann data (faces of type 'N'); None = 0."""
+    def forward(self, b, omega, stream=None, omega_n=None, want_lambda=False):
+        """omega_n: [B][D][P] Neumann data (faces of type 'N'); None = 0.  want_lambda: also
+        return the duals lambda* [B][2+5D][P] (mpde.h mpde_solve_fwd_bc layout)."""
         z = torch.empty((self.B, self.M, self.P), dtype=torch.float32, device=self.c.device)
-        mpde_solve_fwd_bc(self.h_, b, omega, omega_n, z, self.stats, stream)
-        return z
+        lam = (torch.empty((self.B, 2 + 5 * self.D, self.P), dtype=torch.float32, device=self.c.device)
+               if want_lambda else None)
+        mpde_solve_fwd_bc(self.h_, b, omega, omega_n, z, self.stats, stream, lambda_opt=lam)
+        return (z, lam) if want_lambda else z
 
     def backward(self, b, z, g, want_dz=False, stream=None, want_grad_omega_n=False):
         """-> (grad_c, grad_b, grad_omega, dz) or, with want_grad_omega_n, the same plus

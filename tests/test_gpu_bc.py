@@ -3,7 +3,7 @@ Neumann ... or mixed types"; reading B1 in DESIGN.md): per-face Dirichlet / Neum
 rows through the C ABI (mpde_problem.bc, mpde_solve_fwd_bc / _bwd_bc) against the oracle on
 the same inputs -- the normal operator, the condensed operator S, fwd + bwd with every
 gradient including dl/domega_n, and manufactured solutions with Neumann data at grid sizes
-that run the production kernels (two-pass and t-marching) on several levels."""
+that run the production kernels on several levels, and the exported duals lambda*."""
 import numpy as np
 import pytest
 import torch
@@ -144,8 +144,8 @@ def _quad_fields(shape, h, rng):
 @pytest.mark.parametrize("shape,h,bc,B", [((32, 64, 64), (0.01, 1 / 64, 1 / 64), MIXED3, 19),
                                           ((101, 256), (0.1, 1 / 16), MIXED2, 2)])
 def test_manufactured_neumann_full_size(shape, h, bc, B):
-    """P2 with Neumann data at C4 / C2 grid sizes (multigrid on every level; at (32,64,64) with
-    19 PDEs the level-0 applies run the t-marching kernel): u per-dim quadratic, omega = u,
+    """P2 with Neumann data at C4 / C2 grid sizes (multigrid on every level, the production
+    level-0 kernels <64,64> / 2D v4): u per-dim quadratic, omega = u,
     omega_n[d] = du/dx_d, so z* = (u, du) exactly.  Tolerance: the north_star 1e-4 (the
     fp32 rounding of the inputs bounds the floor)."""
     import synth
@@ -166,3 +166,51 @@ def test_manufactured_neumann_full_size(shape, h, bc, B):
     for i in range(B):
         assert st[i]["status"] == "converged", st[i]
         assert _rel(z[i].cpu().numpy(), zs[i]) <= E_Z
+
+
+def _oracle_lambda_structured(pr, lam, info):
+    """Map the oracle's dual vector (rows in assemble's order) onto the structured layout of
+    mpde_solve_fwd_bc's lambda_opt: [2 + 5D][P] (mpde.h)."""
+    shape, D, P = tuple(pr.shape), pr.D, pr.P
+    out = np.zeros((2 + 5 * D, P))
+    out[0] = lam[info["eq_rows"]]
+    out[1][info["bnd_points"]] = lam[info["bnd_rows"]]
+    r0 = P + info["bnd_rows"].size
+    for d, side, fp, rr in info["neu"]:
+        out[2 + d][fp] = lam[rr]
+        r0 += rr.size
+    for d in range(D):
+        for k in (1, 2):
+            out[2 + D + 2 * d + (k - 1)] = lam[r0:r0 + P]
+            r0 += P
+    idx = np.unravel_index(np.arange(P), shape)
+    for d in range(D):
+        for j, sel in enumerate((idx[d] <= shape[d] - 2, idx[d] >= 1)):
+            pts = np.flatnonzero(sel)
+            out[2 + 3 * D + 2 * d + j][pts] = lam[r0:r0 + pts.size]
+            r0 += pts.size
+    assert r0 == lam.size
+    return out
+
+
+@pytest.mark.parametrize("shape,h,bc", [((16, 16), (1 / 15, 1 / 15), None), ((12, 14), (0.1, 0.07), MIXED2),
+                                        ((8, 9, 10), (0.1, 0.07, 0.05), MIXED3)])
+def test_duals_match_oracle(shape, h, bc):
+    """lambda* = d - A z* (Eq. 10 first block row) exported by the forward, against
+    the oracle's lambda* mapped onto the structured layout; judged in absolute terms relative
+    to ||d|| (lambda* -> 0 on consistent systems)."""
+    from paper_2502_18377_b200 import mpde
+    B = 2
+    c, b, om, omn, _ = _problem(shape, B, 6)
+    s = mpde.Solver(shape, h, _dev(c), weights=W, bc=bc)
+    z, lam = s.forward(_dev(b), _dev(om), omega_n=_dev(omn), want_lambda=True)
+    torch.cuda.synchronize()
+    s.close()
+    pr = Problem(shape, h, *W, bc=bc)
+    for i in range(B):
+        f = solve_forward(pr, c[i], b[i], om[i], method="dense" if pr.n_v <= 5000 else "lu",
+                          omega_n=omn[i] if bc is not None else None)
+        ref = _oracle_lambda_structured(pr, f["lam"], f["info"])
+        got = lam[i].cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(got - ref) <= 1e-4 * np.linalg.norm(f["d"]), \
+            (np.linalg.norm(got - ref), np.linalg.norm(f["d"]))
