@@ -290,7 +290,8 @@ def _slab_blocks(shape, M, T):
 
 
 def solve_normal(A, rhs, method: str = "auto", tol: float = 1e-12, maxiter: int = 200000,
-                 info: dict | None = None, strict: bool = True, shape=None, slab: int = 2):
+                 info: dict | None = None, strict: bool = True, shape=None, slab: int = 2,
+                 log=None):
     """Solve A^T A x = rhs (Eq. 9).
 
     method: 'dense' (SVD), 'lu' (SuperLU on S A^T A S + 2 fp64 refinement steps with
@@ -301,8 +302,9 @@ def solve_normal(A, rhs, method: str = "auto", tol: float = 1e-12, maxiter: int 
     block factorised by SuperLU; `shape` = grid shape).  'slab' converges where 'cg' needs
     10^5 iterations (3D, transport-dominated C4 backward); the preconditioner only changes
     the speed: the stop test is the same true normal residual.  Iterative methods stop at
-    rel_res <= tol, or when the true residual stagnates at the fp64 rounding floor; with
-    strict=True an answer whose rel_res exceeds STRICT_REL_RES raises.
+    rel_res <= tol, or when the true residual stagnates at the fp64 rounding floor (no halving
+    within 150 iterations); with strict=True an answer whose rel_res exceeds STRICT_REL_RES
+    raises.  log: optional callable receiving (iteration, rel_res) every 25 iterations.
     """
     n_v = A.shape[1]
     if method == "auto":
@@ -356,13 +358,15 @@ def solve_normal(A, rhs, method: str = "auto", tol: float = 1e-12, maxiter: int 
             if it % 25 == 0:
                 rel = np.linalg.norm(rhs - N @ (s * y)) / nrm
                 hist.append((it, float(rel)))
+                if log is not None:
+                    log(it, float(rel))
                 if rel <= tol:
                     break
                 if rel < 0.5 * best:
                     best, since = rel, 0
                 else:
                     since += 25
-                    if since >= 100 and best <= STRICT_REL_RES:  # fp64 rounding floor reached
+                    if since >= 150:  # the true residual stopped halving: fp64 rounding floor
                         break
             zv = prec(r)
             rz_new = r @ zv

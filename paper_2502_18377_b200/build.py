@@ -7,7 +7,7 @@ import sys
 from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", f) for f in ("kernels.cu", "schur.cu", "dense.cu", "template.cu", "fgmres.cu", "march.cu", "mpde.cu")]
+SRC = [os.path.join(HERE, "csrc", f) for f in ("kernels.cu", "schur.cu", "dense.cu", "template.cu", "fgmres.cu", "march.cu", "slab.cu", "mpde.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "internal.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "mpde.h")]
 OUT = os.path.join(HERE, "libmpde.so")

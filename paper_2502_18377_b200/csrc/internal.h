@@ -130,7 +130,17 @@ int schur_tiles(const Geo& G, bool f64, int nvec);
 // true when this level applies S with the single fused kernel (launch_schur_fused)
 bool schur_fused(const Geo& G, bool f64);
 // one-kernel t-marching S apply (march.cu): 3D fp32 levels with n_y in {32,64,128}, n_x = 8k
-bool use_march(const Geo& G, bool f64, int nvec);  // also needs 16-byte aligned x
+bool use_march(const Geo& G, bool f64, int nvec);
+// mid-size 3D levels (x-y plane <= 1024 points, n_t = 8..32): one launch, a cluster of t-slab
+// CTAs per vector exchanging the t halo through distributed shared memory (slab.cu)
+bool use_slab(const Geo& G, bool f64);
+int slab_ctas(const Geo& G);
+void launch_schur_slab(int epi, const Geo& G, int nvec, int crep, const void* cf, bool bf16,
+                       const float* x, const EpiArgs& A, const int* act, cudaStream_t s);
+// small levels (P <= 4096 per vector): both passes in one launch, one CTA per vector
+bool use_small_fused(const Geo& G, bool f64);
+void launch_schur_small(int epi, const Geo& G, int nvec, int crep, const float* cf, const float* x,
+                        const EpiArgs& A, const int* act, cudaStream_t s);  // also needs 16-byte aligned x
 int march_ctas(const Geo& G);
 void launch_schur_march(int epi, const Geo& G, int nvec, int crep, const void* cf, bool bf16,
                         const float* x, const EpiArgs& A, const int* act, cudaStream_t s);

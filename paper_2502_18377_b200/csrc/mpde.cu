@@ -540,6 +540,18 @@ int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const flo
     CKL();
     return MPDE_OK;
   }
+  if (use_slab(lv.G, f64)) {  // mid-size level: one launch, t-slab clusters (slab.cu)
+    const bool bf = lv.cf16 && crep == 1 &&
+                    (epi == EPI_RESID || epi == EPI_SMOOTH || epi == EPI_SMOOTH_LAST || epi == EPI_POST0);
+    PROF(c_out, s, launch_schur_slab(epi, lv.G, nvec, crep, bf ? lv.cf16 : (const void*)cf, bf, x, A2, act, s));
+    CKL();
+    return MPDE_OK;
+  }
+  if (use_small_fused(lv.G, f64)) {  // small level: one launch, both passes in shared memory
+    PROF(c_out, s, launch_schur_small(epi, lv.G, nvec, crep, cf, x, A2, act, s));
+    CKL();
+    return MPDE_OK;
+  }
   if (schur_fused(lv.G, f64)) {
     PROF(c_out, s, launch_schur_fused(epi, lv.G, nvec, crep, cf, x, A2, act, s));
     CKL();
@@ -1105,6 +1117,16 @@ size_t mpde_workspace_bytes(const mpde_problem* prob, const mpde_options* opts) 
   return plan_workspace(prob, opts, nullptr, nullptr);
 }
 
+// seed of the Lanczos start vector (the same vector for every PDE of a batch); env MPDE_LZ_SEED
+static uint32_t lz_seed() {
+  static long long s = -1;
+  if (s < 0) {
+    const char* e = getenv("MPDE_LZ_SEED");
+    s = e ? atoll(e) : 12345;
+  }
+  return (uint32_t)s;
+}
+
 int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, const float* coeff,
                          void* workspace, size_t workspace_bytes, mpde_stream_t stream_,
                          mpde_hierarchy** out) {
@@ -1202,7 +1224,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
     float* v = lv.d;
     float* vp = lv.pe;
     float* y = lv.d2;
-    launch_rand_fill(lv.P, B, v, 12345u + l, s);
+    launch_rand_fill(lv.P, B, v, lz_seed() + l, s);
     CK(cudaMemsetAsync(vp, 0, sizeof(float) * (size_t)B * lv.P, s));
     launch_scalar(SC_LZ_RESET, B, sl, h->part, nt, 0.f, 0, s);
     launch_lz_update(lv.P, B, v, v, v, lv.dinv, h->st.alpha, h->st.beta, h->part, s);

@@ -205,6 +205,90 @@ __global__ void __launch_bounds__(kThreads) k_schur_s(Geo G, const float* __rest
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Small levels (P <= kSmallFusedP points per vector, e.g. the (8,16,16) level of C4): both
+// passes in ONE launch, one CTA per vector.  x is staged in shared memory, h is computed for
+// every point into shared memory, one barrier, then S x with the fused epilogue.  The
+// two-pass kernels need two launches of a few thousand points each on these levels, which
+// are launch-latency bound (round-1 launch list: ~10 us per coarse pass for 65 k points).
+// ---------------------------------------------------------------------------------
+constexpr int kSmallFusedP = 4096;
+constexpr int kSmallFusedThreads = 512;
+
+template <int EPI>
+__device__ __forceinline__ double point_epilogue(const EpiArgs& A, int pde, size_t o, float xo, float q) {
+  double dot = 0.0;
+  if (EPI == EPI_STORE) {
+    A.y[o] = q;
+  } else if (EPI == EPI_DOT) {
+    A.y[o] = q;
+    dot = double(xo) * q;
+  } else if (EPI == EPI_POWER) {
+    A.y[o] = A.dinv[o] * q;
+    dot = double(xo) * q;
+  } else if (EPI == EPI_RESID) {
+    A.res[o] = A.res[o] - q;
+  } else if (EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST) {
+    const float al = A.coef[pde * A.coef_stride + 2 * A.step];
+    const float be = A.coef[pde * A.coef_stride + 2 * A.step + 1];
+    const float res = A.res[o] - q;
+    const float dn = al * xo + be * A.dinv[o] * res;
+    const float e = A.e[o] + dn;
+    A.e[o] = e;
+    if (EPI == EPI_SMOOTH) {
+      A.res[o] = res;
+      A.d_out[o] = dn;
+    }
+    if (A.rdot) dot = double(A.rdot[o]) * e;
+  } else if (EPI == EPI_POST0) {
+    const float be = A.coef[pde * A.coef_stride + 1];
+    const float res = A.res[o] - q;
+    const float dn = be * A.dinv[o] * res;
+    const float e = A.e[o] + xo + dn;
+    A.e[o] = e;
+    A.res[o] = res;
+    A.d_out[o] = dn;
+    if (A.rdot) dot = double(A.rdot[o]) * e;
+  }
+  return dot;
+}
+
+template <int D, int EPI>
+__global__ void __launch_bounds__(kSmallFusedThreads) k_schur_small(Geo G, const float* __restrict__ cf,
+                                                                   int crep, const float* __restrict__ x,
+                                                                   EpiArgs A, const int* act) {
+  MPDE_PDL_ENTRY();
+  constexpr int NC = 2 + 2 * D;
+  extern __shared__ __align__(16) float ssm[];
+  const int v = blockIdx.x, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  float* xs = ssm;       // [P]
+  float* hs = ssm + P;   // [P]
+  const float* xb = x + (size_t)v * P;
+  const float* cb = cf + (size_t)pde * NC * P;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) xs[p] = xb[p];
+  __syncthreads();
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    int idx[D];
+    unravel<D>(G, p, idx);
+    hs[p] = schur_h_point<D, float>(G, cb, xs, p, idx);
+  }
+  __syncthreads();
+  double dot = 0.0;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    int idx[D];
+    unravel<D>(G, p, idx);
+    const float q = schur_s_point<D, float>(G, cb, xs, hs, p, idx);
+    dot += point_epilogue<EPI>(A, pde, (size_t)v * P + p, xs[p], q);
+  }
+  if (A.pts && threadIdx.x == 0) atomicAdd(A.pts + EPI, (unsigned long long)P);
+  if (EPI == EPI_DOT || EPI == EPI_POWER ||
+      ((EPI == EPI_SMOOTH || EPI == EPI_SMOOTH_LAST || EPI == EPI_POST0) && A.rdot)) {
+    dot = block_sum(dot);
+    if (threadIdx.x == 0) A.part[v] = dot;
+  }
+}
+
 // 1/diag(S) (smoother diagonal), fp64: diag = sum_d P0_d(i,i) + w_bnd^2 [B]
 //   + (sigma alpha) dh(p)/dx(p) - sum_d sum_o sum_k KT[o][k] u~_dk(q) dh(q)/dx(p), q = p + o e_d
 template <int D>
@@ -1862,7 +1946,10 @@ static int schur_tiles2p(const Geo& G, bool f64) {
 }
 
 int schur_tiles(const Geo& G, bool f64, int nvec) {
-  return use_march(G, f64, nvec) ? march_ctas(G) : schur_tiles2p(G, f64);
+  if (use_march(G, f64, nvec)) return march_ctas(G);
+  if (use_slab(G, f64)) return slab_ctas(G);
+  if (use_small_fused(G, f64)) return 1;
+  return schur_tiles2p(G, f64);
 }
 
 void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const float* x, void* g,
@@ -2052,6 +2139,37 @@ void launch_schur_out_bf(int epi, const Geo& G, int nvec, int crep, const void* 
 #undef V4BF
 }
 
+// small levels: one fused launch per apply (env MPDE_SMALL_FUSED=1 enables; at C4 level 2 it
+// took 22 us per apply against ~22 us for the two passes -- one CTA per PDE is too little parallelism)
+static int g_small_fused = -1;
+bool use_small_fused(const Geo& G, bool f64) {
+  if (g_small_fused < 0) {
+    const char* e = getenv("MPDE_SMALL_FUSED");
+    g_small_fused = e ? atoi(e) : 0;  // opt-in: one CTA per PDE measured slower than the two passes
+  }
+  return g_small_fused && !f64 && G.P <= kSmallFusedP;
+}
+
+void launch_schur_small(int epi, const Geo& G, int nvec, int crep, const float* cf, const float* x,
+                        const EpiArgs& A, const int* act, cudaStream_t s) {
+  ++g_launch_count;
+  const size_t smem = sizeof(float) * 2 * (size_t)G.P;
+#define SMALL_CASE(E)                                                                             \
+  case E:                                                                                         \
+    DISPATCH_D2(G.D, (k_schur_small<DD, E><<<nvec, kSmallFusedThreads, smem, s>>>(G, cf, crep, x, A, act))); \
+    break;
+  switch (epi) {
+    SMALL_CASE(EPI_STORE)
+    SMALL_CASE(EPI_DOT)
+    SMALL_CASE(EPI_POWER)
+    SMALL_CASE(EPI_RESID)
+    SMALL_CASE(EPI_SMOOTH)
+    SMALL_CASE(EPI_SMOOTH_LAST)
+    SMALL_CASE(EPI_POST0)
+  }
+#undef SMALL_CASE
+}
+
 void launch_schur_fused(int epi, const Geo& G, int nvec, int crep, const float* cf,
                         const float* x, const EpiArgs& A, const int* act, cudaStream_t s) {
   ++g_launch_count;
@@ -2086,7 +2204,8 @@ void launch_schur_fused(int epi, const Geo& G, int nvec, int crep, const float* 
 //   out[2] pass 2 of the V-cycle applies, out[3] 1 if those read bf16 coefficients.
 // Codes: 0 scalar, 1 v4, 2 v4 warp-specialised, 3 t-blocked (runtime extents),
 // 4 t-blocked (compile-time extents), 5 2x2-blocked, 6 smem tile, 7 fused, 8 pass 1 with y part,
-// 9 one-kernel t-marching apply (march.cu).
+// 9 one-kernel t-marching apply (march.cu), 10 one-CTA-per-vector fused apply (small levels),
+// 11 one-launch t-slab cluster apply (slab.cu, mid-size levels).
 static int pass2_kind(const Geo& G, bool f64) {
   if (use_fused(G, f64)) return 7;
   if (use_tile(G, f64)) return 6;
@@ -2099,6 +2218,16 @@ static int pass2_kind(const Geo& G, bool f64) {
   return 0;
 }
 void schur_variants(const Geo& G, bool f64, bool bf16_level, int nvec, int32_t out[4]) {
+  if (use_slab(G, f64) && !use_march(G, f64, nvec)) {  // one launch per apply, t-slab clusters
+    out[0] = out[1] = out[2] = 11;
+    out[3] = bf16_level ? 1 : 0;
+    return;
+  }
+  if (use_small_fused(G, f64) && !use_march(G, f64, nvec)) {  // one launch per apply, fp32 cf
+    out[0] = out[1] = out[2] = 10;
+    out[3] = 0;
+    return;
+  }
   if (use_march(G, f64, nvec)) {  // one kernel for every apply; V-cycle applies read bf16 cf if kept
     out[0] = out[1] = out[2] = 9;
     out[3] = bf16_level ? 1 : 0;

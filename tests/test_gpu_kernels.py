@@ -73,14 +73,18 @@ np.save(sys.argv[3], np.array(mpde.mpde_hierarchy_query(s.h_, 0, 5, None)))
 # levels above MPDE_SMALLP = 16384 points per vector select the production kernels; below it
 # the 64-thread v4 kernels run whatever the switches say, so the variant cases set
 # MPDE_SMALLP=0 and every case asserts the kernel that actually ran.
-_NOSMALL = {"MPDE_SMALLP": "0", "MPDE_MARCH": "0"}
+_NOSMALL = {"MPDE_SMALLP": "0", "MPDE_MARCH": "0", "MPDE_SMALL_FUSED": "0", "MPDE_SLAB": "0"}
 _NOMARCH = {"MPDE_MARCH": "0"}
 _MARCH = {"MPDE_MARCH": "2"}  # the march on every eligible level, whatever the grid size
 @pytest.mark.parametrize("shape,h,env,kinds,B", [
     # production: the one-kernel t-marching apply (code 9, march.cu) on launches with >= 148 CTAs
     ((6, 64, 64), (0.01, 1 / 64, 1 / 64), {"MPDE_MARCH": "1"}, (9, 9), 19),  # C4 level-0 geometry, 152 CTAs
     ((6, 64, 64), (0.01, 1 / 64, 1 / 64), {}, (1, 4), 19),     # default: two-pass <64,64>
-    ((20, 32, 32), (0.02, 1 / 32, 1 / 32), {}, (1, 4), 2),      # small launch: two-pass <32,32>
+    ((20, 32, 32), (0.02, 1 / 32, 1 / 32), {"MPDE_SLAB": "1"}, (11, 11), 2),    # mid-size level: t-slab clusters (5 CTAs)
+    ((16, 32, 32), (0.02, 1 / 32, 1 / 32), {"MPDE_SLAB": "1"}, (11, 11), 3),    # C4 level-1 geometry (4-CTA clusters)
+    ((32, 32, 32), (0.05, 0.3125, 0.3125), {"MPDE_SLAB": "1"}, (11, 11), 2),    # C3 level-0 geometry (8-CTA clusters)
+    ((12, 24, 40), (0.03, 0.04, 0.02), {"MPDE_SLAB": "1"}, (11, 11), 2),        # 3 slabs, 960-point planes
+    ((20, 32, 32), (0.02, 1 / 32, 1 / 32), {}, (1, 4), 2),      # default: two-pass <32,32>
     ((20, 32, 32), (0.02, 1 / 32, 1 / 32), _MARCH, (9, 9), 2),  # NY 32, 4 strips
     ((7, 16, 64), (0.05, 0.06, 0.07), _MARCH, (9, 9), 2),       # 2 strips, both edge strips
     ((9, 24, 32), (0.05, 0.06, 0.07), _MARCH, (9, 9), 2),       # 3 strips, one interior strip
@@ -90,6 +94,9 @@ _MARCH = {"MPDE_MARCH": "2"}  # the march on every eligible level, whatever the 
     ((6, 64, 64), (0.01, 1 / 64, 1 / 64), _NOMARCH, (1, 4), 2), # t-blocked pass 2 <64,64>
     ((6, 128, 128), (0.005, 1 / 128, 1 / 128), {}, (1, 4), 2),  # C5 level 0: 16 strips > 8, <128,128>
     ((17, 24, 48), (0.05, 0.06, 0.07), {}, (1, 3), 2),          # runtime extents (NY4 = 12, no remap)
+    ((6, 16, 16), (0.05, 0.06, 0.07), {"MPDE_SMALL_FUSED": "1"}, (10, 10), 3),  # small level, one CTA per PDE
+    ((7, 16, 32), (0.05, 0.06, 0.07), {"MPDE_SMALL_FUSED": "1"}, (10, 10), 2),  # P = 3584 (opt-in kernel)
+    ((8, 16, 16), (0.05, 0.06, 0.07), {"MPDE_SLAB": "1"}, (11, 11), 3),         # C4 level-2 geometry: 2-CTA t-slab clusters
     ((7, 16, 32), (0.05, 0.06, 0.07), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7), 2),  # fused, 2 x-tiles
     ((9, 24, 36), (0.04, 0.03, 0.05), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7), 2),  # fused, interior tile
     ((7, 16, 64), (0.05, 0.06, 0.07), _NOSMALL, (1, 3), 2),      # t-blocked, warp-specialised y (NY4=16)
@@ -147,7 +154,7 @@ def test_vcycle_symmetric_positive(shape, h, B):
     s = mpde.Solver(shape, h, torch.from_numpy(c.astype(np.float32)).cuda())
     if P > 16384 and D == 3:
         v = mpde.mpde_hierarchy_query(s.h_, 0, 5, None)
-        want = 4  # t-blocked <n,n> (the t-marching apply is opt-in, MPDE_MARCH)
+        want = 4  # t-blocked <n,n> (the t-slab and t-marching applies are opt-in)
         assert v[2] == want and v[3] == 1, v  # reading bf16 coefficients
     a = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()
     b = torch.from_numpy(rng.normal(size=(B, P)).astype(np.float32)).cuda()

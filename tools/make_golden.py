@@ -34,9 +34,22 @@ def one(item):
     g = synth.make_g(name, 1, start=idx)[0].reshape(-1).astype(np.float64)
     pr = Problem(cfg.shape, cfg.h)
     t0 = time.perf_counter()
+    from oracle import neurlp
+    logf = open(os.path.join(OUT, f"{name.lower()}_pde{idx}.log"), "w")
+    orig = neurlp.solve_normal
+
+    def logged(*a, **kw):  # progress lines + no strict raise: the residual reached is recorded
+        kw["log"] = lambda it, rel: (logf.write(f"{it} {rel:.3e}\n"), logf.flush())
+        kw["strict"] = False
+        kw["maxiter"] = 3000
+        return orig(*a, **kw)
+
+    neurlp.solve_normal = logged
     f = solve_forward(pr, bt["c"][0], bt["b"][0], bt["omega"][0], method="slab", slab=SLAB[name])
     t1 = time.perf_counter()
+    logf.write("bwd\n")
     bw = solve_backward(pr, f, g, method="slab", slab=SLAB[name])
+    neurlp.solve_normal = orig
     t2 = time.perf_counter()
     f32 = lambda a: np.asarray(a, dtype=np.float32)
     base = os.path.join(OUT, f"{name.lower()}_pde{idx}")
