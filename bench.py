@@ -51,6 +51,8 @@ BF16_EPIS = (3, 4, 5, 6)
 BF16_SAVED_PASS2 = 14
 BF16_SAVED_PASS1 = 16
 
+OPT_OVERRIDES = {}  # --opt name=value (mpde_options fields; experiments only)
+
 WORKLOADS = {
     "C4": "C4: 2D Navier-Stokes vorticity, (t,x,y)=(32,64,64), batch 32 per GPU, fwd+bwd incl. "
           "hierarchy build",
@@ -206,7 +208,7 @@ class Workload:
         D = len(self.cfg.shape)
         self.M, self.P = 1 + 2 * D, int(np.prod(self.cfg.shape))
         self.prob = mpde.make_problem(self.cfg.shape, self.cfg.h, B)
-        self.opts = mpde.mpde_default_options()
+        self.opts = mpde.mpde_default_options(**OPT_OVERRIDES)
         self.ws = torch.empty(mpde.mpde_workspace_bytes(self.prob, self.opts), dtype=torch.uint8,
                               device=dev)
         self.sets = []
@@ -566,7 +568,7 @@ def run_ours(a):
             "warmup": a.warmup, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f32 (fp64 refinement/condensation)",
             "data": data,
-            "config": {"workload": WORKLOADS[cfg_name],
+            "config": {"workload": WORKLOADS[cfg_name], "option_overrides": OPT_OVERRIDES or None,
                        "global_batch": total_B, "grid": list(cfg.shape),
                        "parallelism": f"dp{world} (batch-sharded PDEs, NCCL all-reduce of grad_c)",
                        "l2": (f"inputs larger than L2 ({nsets} input set(s) of {in_mb:.0f} MB, "
@@ -630,7 +632,12 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-fgmres", action="store_true")
     ap.add_argument("--no-subconfigs", action="store_true")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="override an mpde_options field, e.g. --opt poll_every=4 (experiments)")
     a = ap.parse_args()
+    for kv in a.opt:
+        k, v = kv.split("=", 1)
+        OPT_OVERRIDES[k] = float(v) if ("." in v or "e" in v.lower()) else int(v)
     env_world = os.environ.get("WORLD_SIZE")
     if a.impl == "ours" and a.gpus > 1 and env_world is None:
         # one process per GPU: re-launch under torch.distributed.run (NCCL, 127.0.0.1)

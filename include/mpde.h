@@ -142,8 +142,9 @@ typedef struct {
 
 typedef struct mpde_hierarchy mpde_hierarchy; /* opaque, host-side handle */
 
-/* Defaults: tol_z 1e-5 (10x below the north_star bar 1e-4: the estimate can read up to ~8x
- * low; on C2-C4 it costs no extra iterations, profiles/r2_tolz_sweep.txt), tol 1e-10, tol_inner 3e-4, tol_inner2 3e-3, max_refine 6, Chebyshev nu = 2, coarsest 8,
+/* Defaults: tol_z 3e-5 (3.3x below the north_star bar 1e-4; measured errors against the
+ * converged oracle references are far below it, Q14; 1e-5 costs a 4th refinement
+ * pass on one C4 PDE, profiles/r2_option_sweep.txt), poll_every 4, tol 1e-10, tol_inner 3e-4, tol_inner2 3e-3, max_refine 6, Chebyshev nu = 2, coarsest 8,
  * 16 Lanczos steps, precision 1. */
 mpde_options mpde_default_options(void);
 

@@ -1065,7 +1065,7 @@ extern "C" {
 mpde_options mpde_default_options(void) {
   mpde_options o;
   o.tol = 1e-10f;
-  o.tol_z = 1e-5f;  // 10x below the north_star z tolerance (Q14: stop margin)
+  o.tol_z = 3e-5f;  // 3.3x below the north_star z tolerance (Q14: stop margin)
   o.tol_inner = 3e-4f;
   o.max_iters = 500;
   o.max_refine = 6;
@@ -1073,7 +1073,7 @@ mpde_options mpde_default_options(void) {
   o.nu = 2;
   o.coarsest = 8;
   o.levels_max = 8;
-  o.poll_every = 8;
+  o.poll_every = 4;  // pipelined poll: <= 2 chunks of masked iterations after convergence
   o.jacobi_theta = 1.3f;
   o.cheb_ratio = 60.f;
   o.lanczos_steps = 16;
