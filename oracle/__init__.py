@@ -22,5 +22,5 @@ Parity status per function:
 from .neurlp import (  # noqa: F401
     Problem, n_fields, field_index, boundary_mask, fd_stencil, assemble, counts,
     lstsq_forward, lstsq_backward, solve_normal, solve_forward, solve_backward,
-    field_gradients, normal_apply,
+    field_gradients, normal_apply, assemble_dh, step_gradient,
 )

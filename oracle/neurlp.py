@@ -484,6 +484,49 @@ def field_gradients(prob: Problem, info, z, lam, dz, dlam):
     return grad_c, grad_b, grad_omega
 
 
+def assemble_dh(prob: Problem, d: int, info) -> sp.csr_matrix:
+    """dA/dh_d: the derivative of the assembly (Eqs. 5-7) with respect to the uniform step of
+    dim d ("step sizes ... are differentiable").  Same row order as `assemble`
+    (info from it); only the derivative rows of dim d (coefficient w_der h^k on z[(d,k),p] ->
+    w_der k h^(k-1)) and the Taylor rows of dim d (+-w_sm h on z[(d,1),p] -> +-w_sm,
+    w_sm h^2/2 on z[(d,2),p] -> w_sm h) depend on h_d."""
+    shape, D, P = tuple(prob.shape), prob.D, prob.P
+    pts = np.arange(P)
+    idx = np.unravel_index(pts, shape)
+    r0 = P + info["bnd_rows"].size + sum(rr.size for _, _, _, rr in info.get("neu", []))
+    rows, cols, vals = [], [], []
+    for dd in range(D):
+        for k in (1, 2):
+            if dd == d:
+                rows.append(r0 + pts)
+                cols.append(field_index(dd, k) * P + pts)
+                vals.append(np.full(P, prob.w_der * k * prob.h[dd] ** (k - 1)))
+            r0 += P
+    for dd in range(D):
+        n = shape[dd]
+        for sgn in (+1, -1):
+            sel = pts[(idx[dd] <= n - 2) if sgn > 0 else (idx[dd] >= 1)]
+            if dd == d:
+                rr = r0 + np.arange(sel.size)
+                rows += [rr, rr]
+                cols += [field_index(dd, 1) * P + sel, field_index(dd, 2) * P + sel]
+                vals += [np.full(sel.size, sgn * prob.w_sm), np.full(sel.size, prob.w_sm * prob.h[dd])]
+            r0 += sel.size
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(r0, prob.n_v))
+
+
+def step_gradient(prob: Problem, fwd: dict, bwd: dict) -> np.ndarray:
+    """dl/dh_d for every dim: the P:240 matrix gradient dA = d_lambda z*^T + lambda* d_z^T
+    contracted with dA/dh_d over A's entries: sum_(r,c) dA_rc (dA/dh_d)_rc."""
+    z, lam, dz, dlam = fwd["z"], fwd["lam"], bwd["dz"], bwd["dlam"]
+    out = np.zeros(prob.D)
+    for d in range(prob.D):
+        J = sp.coo_matrix(assemble_dh(prob, d, fwd["info"]))
+        out[d] = float(np.sum(J.data * (dlam[J.row] * z[J.col] + lam[J.row] * dz[J.col])))
+    return out
+
+
 def solve_backward(prob: Problem, fwd: dict, g, method: str = "auto", tol: float = 1e-12, slab=2):
     """Backward NeuRLP-PDE solve for g = dl/dz* (Eq. 11) and field gradients."""
     sinfo = {}

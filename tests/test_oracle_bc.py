@@ -156,3 +156,40 @@ def test_neumann_heat_converges_to_analytic():
         up = f["z"][:pr.P]
         errs.append(np.linalg.norm(up - u.reshape(-1)) / np.linalg.norm(u))
     assert errs[0] < 1e-3 and errs[1] < errs[0] / 3 and errs[2] < errs[1] / 3.5, errs
+
+
+@pytest.mark.parametrize("shape,h,bc", [((8, 9), (0.1, 0.2), None), ((8, 9), (0.1, 0.2), MIXED2),
+                                        ((6, 7, 8), (0.1, 0.15, 0.12), MIXED3)])
+def test_step_gradient_matches_central_differences(shape, h, bc):
+    """dl/dh_d of l = <g, z*> ("step sizes ... are differentiable"): the P:240 matrix
+    gradient contracted with dA/dh_d (oracle.step_gradient) against central finite differences
+    of the forward solve in h_d; and dA/dh_d itself against the difference quotient of the
+    assembly (its entries are polynomials of degree <= 2 in h_d, so the central quotient is
+    exact up to rounding)."""
+    from oracle import assemble_dh, step_gradient
+    rng = np.random.default_rng(11)
+    pr = Problem(shape, h, 1.3, 2.0, 0.7, 0.9, bc=bc)
+    D = len(shape)
+    c = _rand_c(shape, rng)
+    b = rng.normal(size=pr.P)
+    om = rng.normal(size=pr.P)
+    om_n = rng.normal(size=(D, pr.P)) if bc is not None else None
+    g = rng.normal(size=pr.n_v)
+    f = solve_forward(pr, c, b, om, method="dense", omega_n=om_n)
+    bw = solve_backward(pr, f, g, method="dense")
+    gh = step_gradient(pr, f, bw)
+    for d in range(D):
+        eps = 1e-5 * h[d]
+        hp, hm = list(h), list(h)
+        hp[d] += eps
+        hm[d] -= eps
+        prp = Problem(shape, tuple(hp), 1.3, 2.0, 0.7, 0.9, bc=bc)
+        prm = Problem(shape, tuple(hm), 1.3, 2.0, 0.7, 0.9, bc=bc)
+        Ap, _, _ = assemble(prp, c, b, om, om_n)
+        Am, _, _ = assemble(prm, c, b, om, om_n)
+        J = assemble_dh(pr, d, f["info"])
+        assert abs((Ap - Am) / (2 * eps) - J).max() <= 1e-6 * abs(J).max()
+        lp = g @ solve_forward(prp, c, b, om, method="dense", omega_n=om_n)["z"]
+        lm = g @ solve_forward(prm, c, b, om, method="dense", omega_n=om_n)["z"]
+        fd = (lp - lm) / (2 * eps)
+        assert abs(fd - gh[d]) <= 1e-5 * max(abs(fd), abs(gh[d])), (d, fd, gh[d])
