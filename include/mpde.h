@@ -129,6 +129,9 @@ typedef struct {
                          error: the PCG-calibrated tol_inner2 left e_z 1.5e-4 at C2)       */
   int32_t restart;    /* FGMRES restart length m, 1..32 (default 30; workspace grows by
                          (2m+1) scalar fields per PDE)                                      */
+  int32_t grad_steps; /* 1 = the forward keeps the duals of the derivative and Taylor rows
+                         (4*ndim fields per point of workspace) so that mpde_step_gradient
+                         can return dl/dh after the backward; default 0        */
 } mpde_options;
 
 /* one per PDE, device memory, written by mpde_solve_fwd / mpde_solve_bwd */
@@ -201,6 +204,17 @@ int mpde_solve_bwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* z, con
 int mpde_solve_bwd(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,
                    float* grad_coeff, float* grad_rhs, float* grad_bnd, float* dz_opt,
                    mpde_stats* stats, mpde_stream_t stream);
+
+/* dl/dh_d, the gradient of the loss with respect to the uniform step of every dim (P:114-126:
+ * "step sizes ... are differentiable"), for the loss whose dl/dz* was the g_z of the last
+ * mpde_solve_bwd on this handle: the P:240 matrix gradient d_lambda z*^T + lambda* d_z^T
+ * contracted with dA/dh_d over the derivative rows (coefficient w_der h^k) and Taylor rows
+ * (+-w_sm h, w_sm h^2/2) of dim d.  Needs options.grad_steps = 1 at build (the forward keeps
+ * lambda* of those rows) and the forward and backward of the same (rhs_b, z) on this handle.
+ * z: the forward's output [B][|M|][P] (device); grad_h: [B][ndim] fp32 (device, written).
+ * Deterministic (fixed-order fp64 reduction).  MPDE_ERR_INVALID_ARG without grad_steps or a
+ * preceding forward + backward. */
+int mpde_step_gradient(mpde_hierarchy* h, const float* z, float* grad_h, mpde_stream_t stream);
 
 /* Release the handle (does not free caller memory). */
 int mpde_destroy_hierarchy(mpde_hierarchy* h);

@@ -193,6 +193,10 @@ void launch_gm_scalar(int op, int j, int m, int P, int B, const PdeState& st, co
 void launch_count_active(int B, const int* act, int* out, cudaStream_t s);
 void launch_smooth_coef(int B, int nu, int kind, float theta, float ratio, const double* lmax,
                         float* coef, cudaStream_t s);
+void launch_row_duals(const Geo& G, int B, const double* z64, float* lam, cudaStream_t s);
+int step_grad_tiles(const Geo& G);
+void launch_step_grad(const Geo& G, int B, const float* z, const double* dz64, const float* lam,
+                      double* part, float* grad_h, cudaStream_t s);
 void launch_duals(const Geo& G, int B, const float* c, const float* b, const float* om,
                   const float* omn, const double* z64, float* lam, cudaStream_t s);
 void launch_grad(const Geo& G, int B, const float* c, const float* b, const float* z,

@@ -1054,6 +1054,114 @@ __global__ void __launch_bounds__(kThreads) k_duals(Geo G, const float* __restri
   }
 }
 
+// duals of the derivative rows (d, k) and Taylor rows (d, fwd/bwd) of the forward solution (fp64
+// z*), kept for the step gradient: [B][4D][P], slots 2d+(k-1) then 2D + 2d + {0 fwd, 1 bwd}
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_row_duals(Geo G, const double* __restrict__ z64,
+                                                       float* __restrict__ lam) {
+  MPDE_PDL_ENTRY();
+  constexpr int M = 1 + 2 * D;
+  const int v = blockIdx.y, P = G.P;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int idx[D];
+  unravel<D>(G, p, idx);
+  const double* zb = z64 + (size_t)v * M * P;
+  float* out = lam + (size_t)v * 4 * D * P + p;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const int n = G.n[d], s = G.stride[d], i = idx[d];
+    const double h = G.hd[d], h2 = G.h2d[d];
+    const int cls = fd_cls(i, n), st = fd_start(cls);
+    double D1 = 0.0, D2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const double zv = zb[p + (st + q) * s];
+      D1 += cAd[0][cls][q] * zv;
+      D2 += cAd[1][cls][q] * zv;
+    }
+    const double zd1 = zb[(size_t)(1 + 2 * d) * P + p], zd2 = zb[(size_t)(2 + 2 * d) * P + p];
+    const double z0 = zb[p];
+    out[(size_t)(2 * d) * P] = float(-double(G.wr) * (h * zd1 - D1));
+    out[(size_t)(2 * d + 1) * P] = float(-double(G.wr) * (h2 * zd2 - D2));
+    out[(size_t)(2 * D + 2 * d) * P] = i <= n - 2 ? float(-double(G.ws) * (z0 + h * zd1 + 0.5 * h2 * zd2 - zb[p + s])) : 0.f;
+    out[(size_t)(2 * D + 2 * d + 1) * P] = i >= 1 ? float(-double(G.ws) * (z0 - h * zd1 + 0.5 * h2 * zd2 - zb[p - s])) : 0.f;
+  }
+}
+
+// step gradient, per-point contributions reduced per (PDE, dim, CTA) in fp64: for dim d
+//   sum_k (dlam_der zk + lam_der dzk) w_der k h^(k-1)
+//   + [fwd row] (dlam_f z1 + lam_f dz1) w_sm + (dlam_f z2 + lam_f dz2) w_sm h
+//   + [bwd row] -(dlam_b z1 + lam_b dz1) w_sm + (dlam_b z2 + lam_b dz2) w_sm h
+// with d_lambda = -A d_z of those rows (d_z = the backward's fp64 solution) and lambda* kept
+// by the forward (k_row_duals).
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_step_grad(Geo G, const float* __restrict__ z,
+                                                       const double* __restrict__ dz64,
+                                                       const float* __restrict__ lam,
+                                                       double* __restrict__ part) {
+  MPDE_PDL_ENTRY();
+  constexpr int M = 1 + 2 * D;
+  const int v = blockIdx.y, P = G.P;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  double contrib[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) contrib[d] = 0.0;
+  if (p < P) {
+    int idx[D];
+    unravel<D>(G, p, idx);
+    const double* db = dz64 + (size_t)v * M * P;
+    const float* zb = z + (size_t)v * M * P;
+    const float* lb = lam + (size_t)v * 4 * D * P + p;
+    const double wr = G.wr, ws = G.ws;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int n = G.n[d], s = G.stride[d], i = idx[d];
+      const double h = G.hd[d], h2 = G.h2d[d];
+      const int cls = fd_cls(i, n), st = fd_start(cls);
+      double D1 = 0.0, D2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const double dv = db[p + (st + q) * s];
+        D1 += cAd[0][cls][q] * dv;
+        D2 += cAd[1][cls][q] * dv;
+      }
+      const double d0 = db[p], d1 = db[(size_t)(1 + 2 * d) * P + p], d2 = db[(size_t)(2 + 2 * d) * P + p];
+      const double z1 = zb[(size_t)(1 + 2 * d) * P + p], z2 = zb[(size_t)(2 + 2 * d) * P + p];
+      const double dl1 = -wr * (h * d1 - D1), dl2 = -wr * (h2 * d2 - D2);
+      const double l1 = lb[(size_t)(2 * d) * P], l2 = lb[(size_t)(2 * d + 1) * P];
+      double c = (dl1 * z1 + l1 * d1) * wr + (dl2 * z2 + l2 * d2) * wr * 2.0 * h;
+      if (i <= n - 2) {
+        const double dlf = -ws * (d0 + h * d1 + 0.5 * h2 * d2 - db[p + s]);
+        const double lf = lb[(size_t)(2 * D + 2 * d) * P];
+        c += (dlf * z1 + lf * d1) * ws + (dlf * z2 + lf * d2) * ws * h;
+      }
+      if (i >= 1) {
+        const double dlb = -ws * (d0 - h * d1 + 0.5 * h2 * d2 - db[p - s]);
+        const double lbw = lb[(size_t)(2 * D + 2 * d + 1) * P];
+        c += -(dlb * z1 + lbw * d1) * ws + (dlb * z2 + lbw * d2) * ws * h;
+      }
+      contrib[d] = c;
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double sum = block_sum(contrib[d]);
+    if (threadIdx.x == 0) part[((size_t)v * D + d) * gridDim.x + blockIdx.x] = sum;
+  }
+}
+
+// fixed-order sum of the per-CTA partials: grad_h[v][d]
+__global__ void k_step_grad_reduce(int nvd, int ntiles, const double* __restrict__ part,
+                                   float* __restrict__ out) {
+  MPDE_PDL_ENTRY();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nvd) return;
+  double s = 0.0;
+  for (int t = 0; t < ntiles; ++t) s += part[(size_t)i * ntiles + t];
+  out[i] = float(s);
+}
+
 // out[j] = sum_b x[b][j], fixed summation order (deterministic)
 __global__ void __launch_bounds__(kThreads) k_batch_sum(const float* __restrict__ x, int B,
                                                        int64_t n, float* __restrict__ out) {
@@ -1270,6 +1378,18 @@ void launch_duals(const Geo& G, int B, const float* c, const float* b, const flo
                   const float* omn, const double* z64, float* lam, cudaStream_t s) {
   ++g_launch_count;
   DISPATCH_D(G.D, k_duals<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, c, b, om, omn, z64, lam));
+}
+void launch_row_duals(const Geo& G, int B, const double* z64, float* lam, cudaStream_t s) {
+  ++g_launch_count;
+  DISPATCH_D(G.D, k_row_duals<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, z64, lam));
+}
+int step_grad_tiles(const Geo& G) { return (G.P + kThreads - 1) / kThreads; }
+void launch_step_grad(const Geo& G, int B, const float* z, const double* dz64, const float* lam,
+                      double* part, float* grad_h, cudaStream_t s) {
+  g_launch_count += 2;
+  DISPATCH_D(G.D, k_step_grad<DD><<<grid_for(G.P, B), kThreads, 0, s>>>(G, z, dz64, lam, part));
+  const int nvd = B * G.D;
+  k_step_grad_reduce<<<(nvd + 127) / 128, 128, 0, s>>>(nvd, step_grad_tiles(G), part, grad_h);
 }
 void launch_batch_sum(const float* x, int B, int64_t n, float* out, cudaStream_t s) {
   ++g_launch_count;

@@ -100,6 +100,8 @@ int validate(const mpde_problem* pr, const mpde_options* op) {
     return set_err(MPDE_ERR_INVALID_ARG, "lanczos_steps must be in 2..32");
   if (op->precision < 0 || op->precision > 3)
     return set_err(MPDE_ERR_INVALID_ARG, "precision must be in 0..3");
+  if (op->grad_steps != 0 && op->grad_steps != 1)
+    return set_err(MPDE_ERR_INVALID_ARG, "grad_steps must be 0 or 1");
   if (!(op->tol > 0) || !(op->tol_inner > 0) || !(op->tol_z > 0) || !(op->tol_inner2 > 0))
     return set_err(MPDE_ERR_INVALID_ARG, "tolerances must be > 0");
   return MPDE_OK;
@@ -387,6 +389,9 @@ struct mpde_hierarchy {
   const float* rho_z = nullptr;  // z output of that forward
   unsigned long long fwd_gen = 0;  // forward calls on this handle
   unsigned long long rho_gen = 0;  // generation of the forward that wrote rho
+  float* lamrows = nullptr;        // [B][4D][P] derivative / Taylor row duals (opts.grad_steps)
+  double* sgpart = nullptr;        // [B][D][tiles] step-gradient partials
+  unsigned long long bwd_gen = 0;  // forward generation the last backward followed
   // FGMRES (opts.krylov = 1): basis V [m+1][B][P], preconditioned basis Z [m][B][P]
   float *gmV = nullptr, *gmZ = nullptr;
   double* gmpart = nullptr;  // [B][m+1][gm_tiles(P)]
@@ -470,6 +475,10 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
   h->st.dzprev = bp.take<double>(B);
   h->st.errest = bp.take<double>(B);
   h->d_count = bp.take<int>(2);
+  if (op->grad_steps) {
+    h->lamrows = bp.take<float>((size_t)B * 4 * D * P);
+    h->sgpart = bp.take<double>((size_t)B * D * ((P + kThreads - 1) / kThreads));
+  }
   h->ones = bp.take<int>(B);
   if (op->krylov == 1) {
     const int m = op->restart;
@@ -736,6 +745,7 @@ static std::string graph_key(const mpde_hierarchy* h, int k, int device) {
   key_put(key, o.cf_bf16);
   key_put(key, o.krylov);
   key_put(key, o.restart);
+  key_put(key, o.grad_steps);
   return key;
 }
 
@@ -1083,6 +1093,7 @@ mpde_options mpde_default_options(void) {
   o.krylov = 0;
   o.restart = 30;
   o.tol_inner2 = 3e-3f;  // tools/calib_tol.py: -16% iterations on C4, e_z <= 2.7e-5 on C2-C4
+  o.grad_steps = 0;
   return o;
 }
 
@@ -1290,6 +1301,7 @@ int mpde_solve_fwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* bnd, c
   PROF(10, s, launch_fwd_out(h->lv[0].G, B, h->lv[0].c, rhs_b, h->z64, z, h->rho, s));
   if (lambda_opt)
     PROF(10, s, launch_duals(h->lv[0].G, B, h->lv[0].c, rhs_b, bnd, bnd_n, h->z64, lambda_opt, s));
+  if (h->lamrows) PROF(10, s, launch_row_duals(h->lv[0].G, B, h->z64, h->lamrows, s));
   h->rho_b = rhs_b;
   h->rho_z = z;
   h->rho_gen = ++h->fwd_gen;
@@ -1318,6 +1330,7 @@ int mpde_solve_bwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* z, con
                       h->rho_z == z;
   PROF(10, s, launch_grad(l0.G, B, l0.c, rhs_b, z, rho_ok ? h->rho : nullptr, h->z64,
                           grad_coeff, grad_rhs, grad_bnd, grad_bnd_n, dz_opt, s));
+  h->bwd_gen = rho_ok ? h->fwd_gen : 0;  // step gradient valid for this (forward, backward) pair
   if (stats) launch_stats_out(B, h->st, stats, s);
   CKL();
   return MPDE_OK;
@@ -1328,6 +1341,18 @@ int mpde_solve_bwd(mpde_hierarchy* h, const float* rhs_b, const float* z, const 
                    mpde_stats* stats, mpde_stream_t stream_) {
   return mpde_solve_bwd_bc(h, rhs_b, z, g_z, grad_coeff, grad_rhs, grad_bnd, nullptr, dz_opt, stats,
                            stream_);
+}
+
+int mpde_step_gradient(mpde_hierarchy* h, const float* z, float* grad_h, mpde_stream_t stream_) {
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (!h || !z || !grad_h) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
+  if (!h->lamrows) return set_err(MPDE_ERR_INVALID_ARG, "build with options.grad_steps = 1");
+  if (h->bwd_gen == 0 || h->bwd_gen != h->fwd_gen || z != h->rho_z)
+    return set_err(MPDE_ERR_INVALID_ARG,
+                   "needs the forward and then the backward of the same (rhs_b, z) on this handle");
+  launch_step_grad(h->lv[0].G, h->B, z, h->z64, h->lamrows, h->sgpart, grad_h, s);
+  CKL();
+  return MPDE_OK;
 }
 
 int mpde_apply_normal(const mpde_problem* prob, const float* coeff, const float* z, float* q,

@@ -37,7 +37,8 @@ class mpde_options(C.Structure):
                 ("jacobi_theta", C.c_float), ("cheb_ratio", C.c_float),
                 ("lanczos_steps", C.c_int32), ("precision", C.c_int32),
                 ("use_graphs", C.c_int32), ("tol_z", C.c_float), ("tol_inner2", C.c_float),
-                ("cf_bf16", C.c_int32), ("krylov", C.c_int32), ("restart", C.c_int32)]
+                ("cf_bf16", C.c_int32), ("krylov", C.c_int32), ("restart", C.c_int32),
+                ("grad_steps", C.c_int32)]
 
 
 class mpde_stats(C.Structure):
@@ -72,6 +73,7 @@ def lib():
         L.mpde_solve_fwd.argtypes = [vp, vp, vp, vp, vp, S]
         L.mpde_solve_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, S]
         L.mpde_solve_fwd_bc.argtypes = [vp, vp, vp, vp, vp, vp, vp, S]
+        L.mpde_step_gradient.argtypes = [vp, vp, vp, S]
         L.mpde_solve_bwd_bc.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, S]
         L.mpde_destroy_hierarchy.argtypes = [vp]
         L.mpde_apply_normal.argtypes = [P, vp, vp, vp, S]
@@ -97,7 +99,7 @@ def lib():
 
 
 EXPORTS = ["mpde_default_options", "mpde_sizes", "mpde_workspace_bytes", "mpde_build_hierarchy",
-           "mpde_solve_fwd", "mpde_solve_bwd", "mpde_solve_fwd_bc", "mpde_solve_bwd_bc", "mpde_destroy_hierarchy", "mpde_last_error",
+           "mpde_solve_fwd", "mpde_solve_bwd", "mpde_solve_fwd_bc", "mpde_solve_bwd_bc", "mpde_step_gradient", "mpde_destroy_hierarchy", "mpde_last_error",
            "mpde_apply_normal", "mpde_apply_schur", "mpde_apply_precond", "mpde_hierarchy_query",
            "mpde_host_staging_bytes", "mpde_fwd_bwd_host", "mpde_batch_sum",
            "mpde_profile_begin", "mpde_profile_end", "mpde_launch_count", "mpde_template_terms",
@@ -198,6 +200,13 @@ def mpde_solve_bwd_bc(h, rhs_b, z, g_z, grad_coeff, grad_rhs, grad_bnd, grad_bnd
     _check(lib().mpde_solve_bwd_bc(h, _ptr(rhs_b), _ptr(z), _ptr(_dev_f32(g_z, "g_z")),
                                    _ptr(grad_coeff), _ptr(grad_rhs), _ptr(grad_bnd),
                                    _ptr(grad_bnd_n), _ptr(dz), _ptr(stats), _stream(stream)))
+
+
+def mpde_step_gradient(h, z, grad_h, stream=None):
+    """dl/dh [B][ndim] after mpde_solve_bwd (options.grad_steps = 1)."""
+    _check(lib().mpde_step_gradient(h, _ptr(_dev_f32(z, "z")), _ptr(_dev_f32(grad_h, "grad_h")),
+                                    _stream(stream)))
+    return grad_h
 
 
 def mpde_destroy_hierarchy(h):
@@ -341,6 +350,11 @@ class Solver:
         if want_grad_omega_n:
             return gc, gb, gw, dz, gwn
         return gc, gb, gw, dz
+
+    def step_gradient(self, z, stream=None):
+        """dl/dh_d [B][D] for the last backward (needs opts.grad_steps = 1)."""
+        gh = torch.empty((self.B, self.D), dtype=torch.float32, device=self.c.device)
+        return mpde_step_gradient(self.h_, z, gh, stream)
 
     def stats_list(self):
         s = self.stats.cpu()

@@ -214,3 +214,40 @@ def test_duals_match_oracle(shape, h, bc):
         got = lam[i].cpu().numpy().astype(np.float64)
         assert np.linalg.norm(got - ref) <= 1e-4 * np.linalg.norm(f["d"]), \
             (np.linalg.norm(got - ref), np.linalg.norm(f["d"]))
+
+
+@pytest.mark.parametrize("shape,h,bc", [((16, 16), (1 / 15, 1 / 15), None), ((12, 14), (0.1, 0.07), MIXED2),
+                                        ((8, 9, 10), (0.1, 0.07, 0.05), MIXED3)])
+def test_step_gradient_matches_oracle(shape, h, bc):
+    """dl/dh_d (differentiable step sizes) through mpde_step_gradient against the
+    oracle's P:240 contraction with dA/dh_d (itself pinned by central differences,
+    tests/test_oracle_bc.py)."""
+    from oracle import step_gradient
+    from paper_2502_18377_b200 import mpde
+    B = 2
+    c, b, om, omn, g = _problem(shape, B, 8)
+    s = mpde.Solver(shape, h, _dev(c), weights=W, bc=bc, opts=mpde.mpde_default_options(grad_steps=1))
+    bd = _dev(b)
+    z = s.forward(bd, _dev(om), omega_n=_dev(omn))
+    s.backward(bd, z, _dev(g))
+    gh = s.step_gradient(z)
+    torch.cuda.synchronize()
+    s.close()
+    pr = Problem(shape, h, *W, bc=bc)
+    meth = "dense" if pr.n_v <= 5000 else "lu"
+    for i in range(B):
+        f = solve_forward(pr, c[i], b[i], om[i], method=meth, omega_n=omn[i] if bc is not None else None)
+        bw = solve_backward(pr, f, g[i].reshape(-1).astype(np.float64), method=meth)
+        ref = step_gradient(pr, f, bw)
+        assert _rel(gh[i].cpu().numpy(), ref) <= E_G, (gh[i].cpu().numpy(), ref)
+
+
+def test_step_gradient_requires_option():
+    from paper_2502_18377_b200 import mpde
+    c, b, om, _, g = _problem((12, 14), 1, 9)
+    s = mpde.Solver((12, 14), (0.1, 0.07), _dev(c))
+    z = s.forward(_dev(b), _dev(om))
+    s.backward(_dev(b), z, _dev(g))
+    with pytest.raises(RuntimeError):
+        s.step_gradient(z)
+    s.close()
