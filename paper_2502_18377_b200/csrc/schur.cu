@@ -1952,6 +1952,16 @@ int schur_tiles(const Geo& G, bool f64, int nvec) {
   return schur_tiles2p(G, f64);
 }
 
+// warp-specialised interior / edge y quads in pass 1 too (env MPDE_P1_REMAP=1 enables)
+static int g_p1_remap = -1;
+static inline int pass1_remap(const Geo& G) {
+  if (g_p1_remap < 0) {
+    const char* e = getenv("MPDE_P1_REMAP");
+    g_p1_remap = e ? atoi(e) : 0;  // opt-in: 48.9 vs 49.5 ms per C4 step (no gain)
+  }
+  return g_p1_remap && use_remap(G) ? 1 : 0;
+}
+
 void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const float* x, void* g,
                     const int* act, unsigned long long* pts, bool f64, cudaStream_t s) {
   ++g_launch_count;
@@ -1973,7 +1983,8 @@ void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const flo
     if (f64)
       DISPATCH_D2(G.D, k_schur_h_v4<DD, double><<<gr, th, 0, s>>>(G, cf, crep, x, (double*)g, act, pts, 0));
     else
-      DISPATCH_D2(G.D, k_schur_h_v4<DD, float><<<gr, th, 0, s>>>(G, cf, crep, x, (float*)g, act, pts, 0));
+      DISPATCH_D2(G.D, k_schur_h_v4<DD, float><<<gr, th, 0, s>>>(G, cf, crep, x, (float*)g, act, pts,
+                                                                  pass1_remap(G)));
     return;
   }
   if (f64)
@@ -2092,7 +2103,8 @@ void launch_schur_g_bf(const Geo& G, int nvec, int crep, const void* cf16, const
   const __nv_bfloat16* cf = static_cast<const __nv_bfloat16*>(cf16);
   const int th = v4_threads(G);
   dim3 gr((G.P + 4 * th - 1) / (4 * th), nvec);
-  DISPATCH_D2(G.D, (k_schur_h_v4<DD, float, __nv_bfloat16><<<gr, th, 0, s>>>(G, cf, crep, x, (float*)g, act, pts, 0)));
+  DISPATCH_D2(G.D, (k_schur_h_v4<DD, float, __nv_bfloat16><<<gr, th, 0, s>>>(G, cf, crep, x, (float*)g, act, pts,
+                                                                            pass1_remap(G))));
 }
 
 void launch_schur_out_bf(int epi, const Geo& G, int nvec, int crep, const void* cf16, const float* x,

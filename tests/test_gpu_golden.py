@@ -5,7 +5,8 @@ of the oracle (fp64 assembly of Eqs. 3-8, normal equations Eq. 9 / Eq. 11 solved
 block-Jacobi PCG to a true normal residual <= 1e-10, P:240 gradients), written by
 tools/make_golden.py, which calls only oracle/ and synth/.  The GPU side runs the whole batch
 in the launch configuration bench.py times (C4: 32 PDEs, C3: 16 solves, default options) and
-the listed PDEs are compared element-wise over every field:
+the listed PDEs are compared element-wise over every field (the C4 backward reference stops
+at the fp64 floor of its normal residual, 1.1e-9, where ||d_z|| / ||g|| ~ 3e8):
   e_z = ||z_gpu - z_or|| / ||z_or|| <= 1e-4 (north_star), also per field;
   d_z (every field), grad_c, grad_b, grad_omega: relative L2 <= 1e-3 (north_star).
 The loss direction is g = synth.make_g (N(0,1), SURVEY §8(c) direction 1)."""
@@ -60,7 +61,9 @@ def test_full_size_matches_oracle_reference(name, idx, gpu_runs):
     base = os.path.join(GOLD, f"{name.lower()}_pde{idx}")
     ref = np.load(base + ".npz")
     meta = json.load(open(base + ".json"))
-    assert meta["fwd"]["rel_res"] <= 1e-10 and meta["bwd"]["rel_res"] <= 1e-10  # converged oracle
+    # converged oracle: the forward to <= 1e-10; the C4 backward stops at its fp64 floor 1.1e-9
+    # (||d_z|| / ||g|| ~ 3e8: the normal residual's rounding eps ||N|| ||d_z|| / ||g|| is ~1e-9)
+    assert meta["fwd"]["rel_res"] <= 1e-10 and meta["bwd"]["rel_res"] <= 2e-9
     r = gpu_runs[name]
     assert r["stats_f"][idx]["status"] == "converged" and r["stats_b"][idx]["status"] == "converged"
     cfg = synth.CONFIGS[name]
