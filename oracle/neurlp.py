@@ -46,9 +46,20 @@ class Problem:
     w_der: float = 1.0
     w_sm: float = 1.0
     bc: tuple | None = None  # per dim (low face, high face) in {'D', 'N', '-'}; None = all 'D'
+    order: tuple | None = None  # per dim highest derivative variable, 2 or 3; None = all 2
 
     def face_type(self, d: int, side: int) -> str:
         return "D" if self.bc is None else self.bc[d][side]
+
+    def ord(self, d: int) -> int:
+        """Highest derivative order kept as a variable along dim d ("partial derivatives
+        of arbitrary order"; reading O3: 2 by default, 3 for the KdV u_xxx term)."""
+        return 2 if self.order is None else int(self.order[d])
+
+    def field(self, d: int, k: int) -> int:
+        """Field index of the k-th derivative along dim d: phi first, then per dim its
+        derivatives of orders 1 .. ord(d) (= field_index for the default order 2)."""
+        return 1 + sum(self.ord(e) for e in range(d)) + (k - 1)
 
     @property
     def D(self) -> int:
@@ -60,7 +71,7 @@ class Problem:
 
     @property
     def M(self) -> int:
-        return n_fields(self.D)
+        return 1 + sum(self.ord(d) for d in range(self.D))
 
     @property
     def n_v(self) -> int:
@@ -104,6 +115,10 @@ _A_CENTRAL = {1: np.array([1.0, -8.0, 0.0, 8.0, -1.0]) / 12.0,
               2: np.array([-1.0, 16.0, -30.0, 16.0, -1.0]) / 12.0}
 _A_FORWARD = {1: np.array([-25.0, 48.0, -36.0, 16.0, -3.0]) / 12.0,
               2: np.array([35.0, -104.0, 114.0, -56.0, 11.0]) / 12.0}
+# third derivative (reading O3, "arbitrary order"; the KdV term u_xxx of BASELINE C2): the
+# 5-point central and one-sided rules, exact for polynomials of degree <= 4 like the others
+_A_CENTRAL[3] = np.array([-1.0, 2.0, 0.0, -2.0, 1.0]) / 2.0
+_A_FORWARD[3] = np.array([-5.0, 18.0, -24.0, 14.0, -3.0]) / 2.0
 
 
 def fd_stencil(k: int, i: int, n: int):
@@ -122,7 +137,7 @@ def fd_stencil(k: int, i: int, n: int):
     return -np.arange(0, 5), ((-1.0) ** k) * _A_FORWARD[k]
 
 
-def counts(shape, bc=None):
+def counts(shape, bc=None, order=None):
     """(n_v, n_c) of the constraint system, counted row group by row group.
 
     n_c = P (Eq. 3) + |B| (Eq. 4) + 2D P (Eq. 5, one row per derivative variable)
@@ -136,7 +151,8 @@ def counts(shape, bc=None):
     if bc is not None:
         nb += sum(P // shape[d] for d in range(D) for side in (0, 1) if bc[d][side] == "N")
     smooth = sum(2 * (n - 1) * (P // n) for n in shape)
-    return n_fields(D) * P, P + nb + 2 * D * P + smooth
+    nder = 2 * D if order is None else int(sum(order))
+    return (1 + nder) * P, P + nb + nder * P + smooth
 
 
 # ----------------------------------------------------------------------------
@@ -200,17 +216,17 @@ def assemble(prob: Problem, c: np.ndarray, b: np.ndarray, omega: np.ndarray, ome
                 continue
             fp = face_points(shape, d, side)
             rows.append(r0 + np.arange(fp.size))
-            cols.append(field_index(d, 1) * P + fp)
+            cols.append(prob.field(d, 1) * P + fp)
             vals.append(np.full(fp.size, prob.w_bnd))
             dvec.append(prob.w_bnd * (on[d][fp] if on is not None else np.zeros(fp.size)))
             neu.append((d, side, fp, r0 + np.arange(fp.size)))
             r0 += fp.size
 
-    # Derivative rows (Eq. 5), one per (d, k, p).
+    # Derivative rows (Eq. 5), one per (d, k, p), k = 1 .. ord(d).
     for d in range(D):
         n, hd, i_d = shape[d], prob.h[d], idx[d]
-        for k in (1, 2):
-            f = field_index(d, k)
+        for k in range(1, prob.ord(d) + 1):
+            f = prob.field(d, k)
             rows.append(r0 + pts)
             cols.append(f * P + pts)
             vals.append(np.full(P, prob.w_der * hd ** k))
@@ -226,17 +242,21 @@ def assemble(prob: Problem, c: np.ndarray, b: np.ndarray, omega: np.ndarray, ome
             dvec.append(np.zeros(P))
             r0 += P
 
-    # Smoothness rows (Eqs. 6-7), forward then backward, where the neighbour exists.
+    # Smoothness rows (Eqs. 6-7), forward then backward, where the neighbour exists; the Taylor
+    # expansion runs to the dim's highest derivative variable (+-h^3/6 u_ddd when ord = 3).
     for d in range(D):
         n, hd, i_d = shape[d], prob.h[d], idx[d]
-        f1, f2 = field_index(d, 1), field_index(d, 2)
+        f1, f2 = prob.field(d, 1), prob.field(d, 2)
         for sgn in (+1, -1):
             sel = pts[(i_d <= n - 2) if sgn > 0 else (i_d >= 1)]
             rr = r0 + np.arange(sel.size)
             w = prob.w_sm
-            for col, val in ((0 * P + sel, w), (f1 * P + sel, sgn * w * hd),
-                             (f2 * P + sel, 0.5 * w * hd * hd),
-                             (0 * P + sel + sgn * strides[d], -w)):
+            terms = [(0 * P + sel, w), (f1 * P + sel, sgn * w * hd),
+                     (f2 * P + sel, 0.5 * w * hd * hd)]
+            if prob.ord(d) >= 3:
+                terms.append((prob.field(d, 3) * P + sel, sgn * w * hd ** 3 / 6.0))
+            terms.append((0 * P + sel + sgn * strides[d], -w))
+            for col, val in terms:
                 rows.append(rr)
                 cols.append(col)
                 vals.append(np.full(sel.size, val) if np.isscalar(val) else val)
@@ -496,10 +516,10 @@ def assemble_dh(prob: Problem, d: int, info) -> sp.csr_matrix:
     r0 = P + info["bnd_rows"].size + sum(rr.size for _, _, _, rr in info.get("neu", []))
     rows, cols, vals = [], [], []
     for dd in range(D):
-        for k in (1, 2):
+        for k in range(1, prob.ord(dd) + 1):
             if dd == d:
                 rows.append(r0 + pts)
-                cols.append(field_index(dd, k) * P + pts)
+                cols.append(prob.field(dd, k) * P + pts)
                 vals.append(np.full(P, prob.w_der * k * prob.h[dd] ** (k - 1)))
             r0 += P
     for dd in range(D):
@@ -509,8 +529,12 @@ def assemble_dh(prob: Problem, d: int, info) -> sp.csr_matrix:
             if dd == d:
                 rr = r0 + np.arange(sel.size)
                 rows += [rr, rr]
-                cols += [field_index(dd, 1) * P + sel, field_index(dd, 2) * P + sel]
+                cols += [prob.field(dd, 1) * P + sel, prob.field(dd, 2) * P + sel]
                 vals += [np.full(sel.size, sgn * prob.w_sm), np.full(sel.size, prob.w_sm * prob.h[dd])]
+                if prob.ord(dd) >= 3:
+                    rows.append(rr)
+                    cols.append(prob.field(dd, 3) * P + sel)
+                    vals.append(np.full(sel.size, sgn * prob.w_sm * 0.5 * prob.h[dd] ** 2))
             r0 += sel.size
     return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                          shape=(r0, prob.n_v))
