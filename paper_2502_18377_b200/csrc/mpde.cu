@@ -531,9 +531,14 @@ PdeState state_with_lmax(const mpde_hierarchy* h, double* lmax) {
 // the condensation when >= 1, for the V-cycle too when >= 2 (f64_outer / f64_vcycle).
 
 int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const float* x,
-                const EpiArgs& A, const int* act, bool f64, cudaStream_t s) {
+                const EpiArgs& A, const int* act, bool f64, cudaStream_t s, int pde0 = 0) {
+  // pde0: first PDE of this launch (a chunk of the batch, vcycle's level-0 chunking): the
+  // per-point coefficients and the h scratch are offset here, the caller offsets x, A and act
   Level& lv = h->lv[l];
-  const float* cf = lv.cf;
+  const size_t cfo = (size_t)pde0 * (2 + 2 * h->prob.ndim) * lv.P;
+  const float* cf = lv.cf + cfo;
+  const void* cf16 = lv.cf16 ? static_cast<const void*>(static_cast<const uint16_t*>(lv.cf16) + cfo) : nullptr;
+  float* gsc = lv.g + (size_t)pde0 * lv.P * (f64 ? 2 : 1);
   EpiArgs A2 = A;
   // profiling: level 0 has its own classes (11 pass 2, 12 pass 1) and point counters
   A2.pts = g_prof.on ? g_prof.d_pts + (l == 0 ? 9 : 0) : nullptr;
@@ -541,18 +546,18 @@ int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const flo
   // one-kernel t-marching S apply (march.cu): bulk-async plane streaming, DSMEM halo
   // exchange; the V-cycle applies on level 0 read the bf16 coefficients (see below)
   if (use_march(lv.G, f64, nvec) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0)) {
-    const bool bf = lv.cf16 && crep == 1 &&
+    const bool bf = cf16 && crep == 1 &&
                     (epi == EPI_RESID || epi == EPI_SMOOTH || epi == EPI_SMOOTH_LAST || epi == EPI_POST0);
     A2.pts = g_prof.on ? g_prof.d_pts + (l == 0 ? 16 : 24) : nullptr;
     PROF(l == 0 ? 13 : 14, s,
-         launch_schur_march(epi, lv.G, nvec, crep, bf ? lv.cf16 : (const void*)cf, bf, x, A2, act, s));
+         launch_schur_march(epi, lv.G, nvec, crep, bf ? cf16 : (const void*)cf, bf, x, A2, act, s));
     CKL();
     return MPDE_OK;
   }
   if (use_slab(lv.G, f64)) {  // mid-size level: one launch, t-slab clusters (slab.cu)
-    const bool bf = lv.cf16 && crep == 1 &&
+    const bool bf = cf16 && crep == 1 &&
                     (epi == EPI_RESID || epi == EPI_SMOOTH || epi == EPI_SMOOTH_LAST || epi == EPI_POST0);
-    PROF(c_out, s, launch_schur_slab(epi, lv.G, nvec, crep, bf ? lv.cf16 : (const void*)cf, bf, x, A2, act, s));
+    PROF(c_out, s, launch_schur_slab(epi, lv.G, nvec, crep, bf ? cf16 : (const void*)cf, bf, x, A2, act, s));
     CKL();
     return MPDE_OK;
   }
@@ -570,18 +575,18 @@ int schur_apply(mpde_hierarchy* h, int l, int epi, int nvec, int crep, const flo
   // residual use S~ built from rounded coefficients -- still symmetric PSD (S = P0 + M s M^T
   // for any coefficient values), so the preconditioner stays a fixed SPD map; the PCG
   // operator (EPI_DOT) and the refinement keep the fp32 / fp64 coefficients.
-  if (lv.cf16 && !f64 && crep == 1 &&
+  if (cf16 && !f64 && crep == 1 &&
       (epi == EPI_RESID || epi == EPI_SMOOTH || epi == EPI_SMOOTH_LAST || epi == EPI_POST0) &&
       schur_bf16_ok(lv.G, f64)) {
-    PROF(c_g, s, launch_schur_g_bf(lv.G, nvec, crep, lv.cf16, x, lv.g, act,
+    PROF(c_g, s, launch_schur_g_bf(lv.G, nvec, crep, cf16, x, gsc, act,
                                    g_prof.on ? g_prof.d_pts + (l == 0 ? 7 : 8) : nullptr, s));
-    PROF(c_out, s, launch_schur_out_bf(epi, lv.G, nvec, crep, lv.cf16, x, lv.g, A2, act, s));
+    PROF(c_out, s, launch_schur_out_bf(epi, lv.G, nvec, crep, cf16, x, gsc, A2, act, s));
     CKL();
     return MPDE_OK;
   }
-  PROF(c_g, s, launch_schur_g(lv.G, nvec, crep, cf, x, lv.g, act,
+  PROF(c_g, s, launch_schur_g(lv.G, nvec, crep, cf, x, gsc, act,
                               g_prof.on ? g_prof.d_pts + (l == 0 ? 7 : 8) : nullptr, f64, s));
-  PROF(c_out, s, launch_schur_out(epi, lv.G, nvec, crep, cf, x, lv.g, A2, act, f64, s));
+  PROF(c_out, s, launch_schur_out(epi, lv.G, nvec, crep, cf, x, gsc, A2, act, f64, s));
   CKL();
   return MPDE_OK;
 }
@@ -598,11 +603,87 @@ static int wcycle_levels() {
   return w;
 }
 
+// Level-0 work of the V-cycle in chunks of PDEs (env MPDE_L0_CHUNK = PDEs per chunk, 0 = off):
+// the pre-smoothing of a chunk (smooth start, nu-1 smoothing applies, the residual apply and
+// the restriction) runs back to back, so its bf16 coefficients and smoother vectors stay in
+// the 126 MB L2 across those applies instead of streaming the whole batch from HBM each time;
+// the coarse V-cycle then runs on the whole batch, and the prolongation + post-smoothing again
+// chunk by chunk.  Same arithmetic, same order per PDE (bit-identical results).
+static int l0_chunk() {
+  static int c = -1;
+  if (c < 0) {
+    const char* e = getenv("MPDE_L0_CHUNK");
+    c = e ? atoi(e) : 0;  // off: chunks of 16 / 8 / 4 PDEs measured 149 / 130 / 110 vs 159 solves/s
+  }
+  return c;
+}
+
 int vcycle(mpde_hierarchy* h, int l, const float* rin, const float* rdot, double* part,
            const int* act, cudaStream_t s) {
   const int B = h->B;
   Level& lv = h->lv[l];
   const int nu = h->opts.nu;
+  const int Bc = l0_chunk();
+  if (l == 0 && h->L > 1 && Bc > 0 && Bc < B && wcycle_levels() == 0 &&
+      !use_march(lv.G, f64_vcycle(h), Bc) && !use_march(lv.G, f64_vcycle(h), B)) {
+    Level& lc = h->lv[1];
+    const int P = lv.P;
+    const int nt = schur_tiles(lv.G, f64_vcycle(h), B);
+    auto chunk_args = [&](int c0) {
+      EpiArgs A;
+      A.dinv = lv.dinv + (size_t)c0 * P;
+      A.coef = lv.coef + (size_t)c0 * 2 * nu;
+      A.coef_stride = 2 * nu;
+      A.res = lv.r + (size_t)c0 * P;
+      A.e = lv.e + (size_t)c0 * P;
+      return A;
+    };
+    for (int c0 = 0; c0 < B; c0 += Bc) {
+      const int nb = std::min(Bc, B - c0);
+      const size_t o = (size_t)c0 * P;
+      EpiArgs A = chunk_args(c0);
+      PROF(6, s, launch_smooth_start(P, nb, rin + o, lv.dinv + o, lv.coef + (size_t)c0 * 2 * nu, 2 * nu,
+                                     lv.r + o, lv.d + o, lv.e + o, act + c0, s));
+      float* dcur = lv.d;
+      float* dnext = lv.d2;
+      for (int k = 1; k < nu; ++k) {
+        A.step = k;
+        A.d_out = dnext + o;
+        if (int rc = schur_apply(h, 0, EPI_SMOOTH, nb, 1, dcur + o, A, act + c0, f64_vcycle(h), s, c0)) return rc;
+        std::swap(dcur, dnext);
+      }
+      if (int rc = schur_apply(h, 0, EPI_RESID, nb, 1, dcur + o, A, act + c0, f64_vcycle(h), s, c0)) return rc;
+      PROF(5, s, launch_restrict1(lv.G, lc.G, nb, lv.r + o, lc.r + (size_t)c0 * lc.P, act + c0, s));
+      CKL();
+    }
+    if (int rc = vcycle(h, 1, lc.r, nullptr, nullptr, act, s)) return rc;
+    for (int c0 = 0; c0 < B; c0 += Bc) {
+      const int nb = std::min(Bc, B - c0);
+      const size_t o = (size_t)c0 * P;
+      PROF(5, s, launch_prolong1(lv.G, lc.G, nb, lc.e + (size_t)c0 * lc.P, lv.pe + o, act + c0, s));
+      CKL();
+      EpiArgs A = chunk_args(c0);
+      A.step = 0;
+      A.d_out = lv.d + o;
+      A.rdot = (nu == 1 && rdot) ? rdot + o : nullptr;
+      A.part = (nu == 1 && part) ? part + (size_t)c0 * nt : nullptr;
+      if (int rc = schur_apply(h, 0, EPI_POST0, nb, 1, lv.pe + o, A, act + c0, f64_vcycle(h), s, c0)) return rc;
+      float* dcur = lv.d;
+      float* dnext = lv.d2;
+      for (int k = 1; k < nu; ++k) {
+        const bool last = (k == nu - 1);
+        A.step = k;
+        A.d_out = dnext + o;
+        A.rdot = (last && rdot) ? rdot + o : nullptr;
+        A.part = (last && part) ? part + (size_t)c0 * nt : nullptr;
+        if (int rc = schur_apply(h, 0, last ? EPI_SMOOTH_LAST : EPI_SMOOTH, nb, 1, dcur + o, A, act + c0,
+                                   f64_vcycle(h), s, c0))
+          return rc;
+        std::swap(dcur, dnext);
+      }
+    }
+    return MPDE_OK;
+  }
   if (l == h->L - 1) {
     PROF(8, s, launch_coarse_gemv(lv.P, B, h->sinv, rin, lv.e, rdot, part, act, s));
     CKL();

@@ -641,7 +641,7 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const CF* __restrict__ cb
 }
 
 template <int D, typename T, typename CF = float>
-__global__ void __launch_bounds__(kThreads) k_schur_h_v4(Geo G, const CF* __restrict__ cf, int crep,
+__global__ void __launch_bounds__(kThreads, 5) k_schur_h_v4(Geo G, const CF* __restrict__ cf, int crep,
                                                         const float* __restrict__ x,
                                                         T* __restrict__ hout, const int* act,
                                                         unsigned long long* pts, int remap) {

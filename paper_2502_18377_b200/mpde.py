@@ -17,7 +17,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpde.so")
+LIB_PATH = os.environ.get("MPDE_LIB") or os.path.join(_HERE, "libmpde.so")  # MPDE_LIB: A/B builds
 
 
 class mpde_problem(C.Structure):
