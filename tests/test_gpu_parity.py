@@ -139,11 +139,12 @@ def test_c1_heat_parity(gu):
             assert gu.rel(out[k][0], bw[k]) <= E_G, k
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
-def test_mms_full_size(name, gu):
-    """P2 at the configs' full sizes (C4 = the bench workload, full batch): the closed-form
-    manufactured solution is recovered within 1e-4 by the CUDA path."""
-    m = synth.make_mms(name)
+@pytest.mark.parametrize("name,batch", [("C2", None), ("C3", None), ("C4", None), ("C5", 2)])
+def test_mms_full_size(name, batch, gu):
+    """P2 at the configs' full sizes (C4 = the bench workload, full batch; C5 = the (64,128,128)
+    scaling grid, 2 PDEs): the closed-form manufactured solution is recovered within 1e-4 by
+    the CUDA path."""
+    m = synth.make_mms(name, batch)
     cfg = m["cfg"]
     out = gu.gpu_solve(cfg.shape, cfg.h, m["c"], m["b"], m["omega"])
     errs = [gu.rel(out["z"][i], m["z_exact"][i]) for i in range(m["c"].shape[0])]
