@@ -53,7 +53,7 @@ typedef struct CUstream_st* mpde_stream_t; /* == cudaStream_t; NULL = legacy def
 enum {
   MPDE_OK = 0,
   MPDE_ERR_INVALID_ARG = 1,   /* null pointer, batch < 1, non-finite step, ...        */
-  MPDE_ERR_SHAPE = 2,         /* ndim not in {2,3}, a dim with fewer than 6 points    */
+  MPDE_ERR_SHAPE = 2,         /* ndim not in {2,3,4}, a dim with fewer than 6 points  */
   MPDE_ERR_UNSUPPORTED = 3,   /* deriv_order != 2, unknown smoother/coarse option     */
   MPDE_ERR_NONFINITE = 4,     /* (status only) non-finite input or residual           */
   MPDE_ERR_NOT_CONVERGED = 5, /* (status only) tolerance not met within the limits    */
@@ -72,7 +72,7 @@ enum { MPDE_BC_DIRICHLET = 0, MPDE_BC_NEUMANN = 1, MPDE_BC_NONE = 2 };
 /* Grid, batch and row-group weights.  P:89 (Cartesian grid), P:111-117 (uniform step
  * per dim -- learned per-interval steps are out of scope), P:147-151 (variables). */
 typedef struct {
-  int32_t ndim;        /* grid dims including time: 2 or 3; dim 0 = time (slowest)      */
+  int32_t ndim;        /* grid dims including time: 2, 3 or 4; dim 0 = time (slowest)   */
   int32_t n[4];        /* points per dim, each >= 6 (5-point one-sided edge stencils)   */
   double  h[4];        /* uniform step per dim, finite, > 0                             */
   int32_t batch;       /* B >= 1 independent PDEs                                        */
@@ -240,7 +240,7 @@ int mpde_apply_schur(mpde_hierarchy* h, int32_t level, const float* x, float* y,
 int mpde_apply_precond(mpde_hierarchy* h, const float* r, float* z, mpde_stream_t stream);
 
 /* Copy internal per-level data to the caller (device pointer `dst`):
- *   what = 0: level shape (n0, n1, n2, levels) -> dst is HOST int32[4] (synchronous)
+ *   what = 0: level shape (n0, n1, n2, levels) -> dst is HOST int32[4] (synchronous; 2D/3D)
  *   what = 1: 1/diag(S_l) [B][P_l] fp32        what = 2: lambda_max [B] fp32
  *   what = 3: coarse coefficients [B][|M|][P_l] fp32
  *   what = 4: coarsest-level inverse [B][P_c][P_c] fp32 (level ignored)
@@ -248,7 +248,9 @@ int mpde_apply_precond(mpde_hierarchy* h, const float* r, float* z, mpde_stream_
  *             [pass 1 of the PCG operator, pass 2 of the PCG operator, pass 2 of the V-cycle
  *             applies, 1 if those read bf16 coefficients]; codes 0 scalar, 1 v4, 2 v4
  *             warp-specialised, 3 t-blocked, 4 t-blocked with compile-time extents,
- *             5 2x2-blocked, 6 smem tile, 7 fused, 8 pass 1 with the y part */
+ *             5 2x2-blocked, 6 smem tile, 7 fused, 8 pass 1 with the y part
+ *   what = 6: level shape of any ndim (n0, n1, n2, n3, levels), 0 for dims >= ndim -> dst is
+ *             HOST int32[5] (synchronous) */
 int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* dst,
                          mpde_stream_t stream);
 

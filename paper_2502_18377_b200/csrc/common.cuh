@@ -24,7 +24,7 @@
 
 namespace mpde {
 
-constexpr int kMaxD = 3;
+constexpr int kMaxD = 4;  // grid dims incl. time (mpde.h: ndim 2..4)
 constexpr int kThreads = 256;
 constexpr int kTabRow = 52;  // floats per (axis, index) row of the condensed-operator tables
 constexpr int kTabKf = 0;   // row segments, 16-byte aligned: Kf [0,18), KT [20,38), P0 [40,51)
@@ -95,12 +95,20 @@ __device__ __forceinline__ void unravel(const Geo& G, int p, int* idx) {
   if (D == 2) {
     idx[0] = p / G.n[1];
     idx[1] = p - idx[0] * G.n[1];
-  } else {
+  } else if (D == 3) {
     int nn = G.n[1] * G.n[2];
     idx[0] = p / nn;
     int r = p - idx[0] * nn;
     idx[1] = r / G.n[2];
     idx[2] = r - idx[1] * G.n[2];
+  } else {
+#pragma unroll
+    for (int d = D - 1; d > 0; --d) {
+      const int q = p / G.n[d];
+      idx[d] = p - q * G.n[d];
+      p = q;
+    }
+    idx[0] = p;
   }
 }
 

@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256) k_restrict1(Geo Gf, Geo Gc, const float* 
       for (int b = 0; b < 4; ++b) s += w[D - 1][b] * __ldg(row + f[D - 1][b]);
       acc += w[0][a] * s;
     }
-  } else {
+  } else if (D == 3) {
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       if (w[0][a] == 0.f) continue;
@@ -253,6 +253,21 @@ __global__ void __launch_bounds__(256) k_restrict1(Geo Gf, Geo Gc, const float* 
 #pragma unroll
         for (int c = 0; c < 4; ++c) s += w[2][c] * __ldg(row + f[2][c]);
         acc += w[0][a] * w[1][b] * s;
+      }
+    }
+  } else {  // 4D: the same tensor-product full weighting over the fourth axis
+    for (int a = 0; a < 4; ++a) {
+      if (w[0][a] == 0.f) continue;
+      for (int b = 0; b < 4; ++b) {
+        if (w[1][b] == 0.f) continue;
+        for (int c = 0; c < 4; ++c) {
+          if (w[2][c] == 0.f) continue;
+          const float* row = fb + f[0][a] * Gf.stride[0] + f[1][b] * Gf.stride[1] + f[2][c] * Gf.stride[2];
+          float s = 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s += w[D - 1][e] * __ldg(row + f[D - 1][e]);
+          acc += w[0][a] * w[1][b] * w[2][c] * s;
+        }
       }
     }
   }
@@ -439,7 +454,7 @@ __global__ void __launch_bounds__(256) k_prolong1q(Geo Gf, Geo Gc, const float* 
 // restriction's float4 window)
 static inline bool transfer_quads(const Geo& Gf, const Geo& Gc) {
   const int L = Gf.D - 1;
-  return (Gf.n[L] % 4 == 0) && (Gc.n[L] % 4 == 0);
+  return Gf.D <= 3 && (Gf.n[L] % 4 == 0) && (Gc.n[L] % 4 == 0);  // 4D: the generic kernels
 }
 
 void launch_restrict1(const Geo& Gf, const Geo& Gc, int nvec, const float* fine, float* coarse,
@@ -456,6 +471,8 @@ void launch_restrict1(const Geo& Gf, const Geo& Gc, int nvec, const float* fine,
   const dim3 g((Gc.P + 255) / 256, nvec);
   if (Gf.D == 2)
     k_restrict1<2><<<g, 256, 0, s>>>(Gf, Gc, fine, coarse, act);
+  else if (Gf.D == 4)
+    k_restrict1<4><<<g, 256, 0, s>>>(Gf, Gc, fine, coarse, act);
   else
     k_restrict1<3><<<g, 256, 0, s>>>(Gf, Gc, fine, coarse, act);
 }
@@ -474,6 +491,8 @@ void launch_prolong1(const Geo& Gf, const Geo& Gc, int nvec, const float* coarse
   const dim3 g((Gf.P + 255) / 256, nvec);
   if (Gf.D == 2)
     k_prolong1<2><<<g, 256, 0, s>>>(Gf, Gc, coarse, fine, act);
+  else if (Gf.D == 4)
+    k_prolong1<4><<<g, 256, 0, s>>>(Gf, Gc, coarse, fine, act);
   else
     k_prolong1<3><<<g, 256, 0, s>>>(Gf, Gc, coarse, fine, act);
 }

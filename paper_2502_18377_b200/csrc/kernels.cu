@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict(Geo Gf, Geo Gc, int nfiel
           acc += w0 * w1 * fb[i0 * Gf.stride[0] + i1];
         }
       }
-    } else {
+    } else if (D == 3) {
       for (int a = 0; a < cnt[0]; ++a) {
         const int i0 = lo[0] + a;
         const float w0 = pw(i0, cidx[0], Gf.n[0], Gc.n[0]);
@@ -410,6 +410,27 @@ __global__ void __launch_bounds__(kThreads) k_restrict(Geo Gf, Geo Gc, int nfiel
             const int i2 = lo[2] + c2;
             const float w2 = pw(i2, cidx[2], Gf.n[2], Gc.n[2]);
             acc += w0 * w1 * w2 * fb[i0 * Gf.stride[0] + i1 * Gf.stride[1] + i2];
+          }
+        }
+      }
+    } else {  // 4D
+      for (int a = 0; a < cnt[0]; ++a) {
+        const int i0 = lo[0] + a;
+        const float w0 = pw(i0, cidx[0], Gf.n[0], Gc.n[0]);
+        if (w0 == 0.f) continue;
+        for (int b2 = 0; b2 < cnt[1]; ++b2) {
+          const int i1 = lo[1] + b2;
+          const float w1 = pw(i1, cidx[1], Gf.n[1], Gc.n[1]);
+          if (w1 == 0.f) continue;
+          for (int c2 = 0; c2 < cnt[2]; ++c2) {
+            const int i2 = lo[2] + c2;
+            const float w2 = pw(i2, cidx[2], Gf.n[2], Gc.n[2]);
+            if (w2 == 0.f) continue;
+            for (int e2 = 0; e2 < cnt[D - 1]; ++e2) {
+              const int i3 = lo[D - 1] + e2;
+              const float w3 = pw(i3, cidx[D - 1], Gf.n[D - 1], Gc.n[D - 1]);
+              acc += w0 * w1 * w2 * w3 * fb[i0 * Gf.stride[0] + i1 * Gf.stride[1] + i2 * Gf.stride[2] + i3];
+            }
           }
         }
       }
@@ -1227,15 +1248,18 @@ void upload_constants() {
   done = true;
 }
 
-#define DISPATCH_D(D_, ...)        \
-  do {                             \
-    if ((D_) == 2) {               \
-      constexpr int DD = 2;        \
-      __VA_ARGS__;                 \
-    } else {                       \
-      constexpr int DD = 3;        \
-      __VA_ARGS__;                 \
-    }                              \
+#define DISPATCH_D(D_, ...) \
+  do {                       \
+    if ((D_) == 2) {         \
+      constexpr int DD = 2;  \
+      __VA_ARGS__;           \
+    } else if ((D_) == 3) {  \
+      constexpr int DD = 3;  \
+      __VA_ARGS__;           \
+    } else {                \
+      constexpr int DD = 4;  \
+      __VA_ARGS__;           \
+    }                        \
   } while (0)
 
 void launch_rhs_init(const Geo& G, int B, const float* c, const float* b, const float* om,

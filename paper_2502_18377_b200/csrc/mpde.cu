@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "internal.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost a null check without a tool attached
 
 using namespace mpde;
 
@@ -54,6 +55,15 @@ int set_err(int code, const char* fmt, ...) {
                      cudaGetErrorString(e_));                                         \
   } while (0)
 
+// NVTX ranges around the API calls and refinement passes (SURVEY §5 tracing): visible to
+// nsys / ncu --nvtx; a no-op unless a tool injects the NVTX library.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 constexpr int kMaxLevels = 10;
 
 struct LevelShape {
@@ -63,8 +73,8 @@ struct LevelShape {
 
 int validate(const mpde_problem* pr, const mpde_options* op) {
   if (!pr || !op) return set_err(MPDE_ERR_INVALID_ARG, "null problem/options");
-  if (pr->ndim < 2 || pr->ndim > 3)
-    return set_err(MPDE_ERR_SHAPE, "ndim must be 2 or 3 (got %d)", pr->ndim);
+  if (pr->ndim < 2 || pr->ndim > 4)
+    return set_err(MPDE_ERR_SHAPE, "ndim must be 2, 3 or 4 (got %d)", pr->ndim);
   if (pr->deriv_order != 2)
     return set_err(MPDE_ERR_UNSUPPORTED, "deriv_order must be 2 (got %d)", pr->deriv_order);
   if (pr->batch < 1) return set_err(MPDE_ERR_INVALID_ARG, "batch must be >= 1");
@@ -140,7 +150,10 @@ int plan_levels(const mpde_problem* pr, const mpde_options* op, LevelShape* lv) 
   return L;
 }
 
-constexpr int kMaxCoarse = 1024;  // dense inverse on the coarsest level
+// dense inverse on the coarsest level: 4D grids stop at >= 6^4 = 1296 points (every dim keeps
+// >= 6 for the 5-point edge stencils), so the cap sits above that; the probe / inverse
+// workspace is 28 B x Pc^2 per PDE (mpde_workspace_size)
+constexpr int kMaxCoarse = 4096;
 
 Geo make_geo(const mpde_problem* pr, const LevelShape& s, int level_scale[kMaxD]) {
   Geo G{};
@@ -414,7 +427,7 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
   Bump bp(base);
   mpde_hierarchy tmp;
   mpde_hierarchy* h = H ? H : &tmp;
-  int scale[kMaxD] = {1, 1, 1};
+  int scale[kMaxD] = {1, 1, 1, 1};
   for (int l = 0; l < L; ++l) {
     Level& lv = h->lv[l];
     if (l > 0)
@@ -1126,6 +1139,7 @@ int solve_core(mpde_hierarchy* h, const float* rhs, const float* b, const float*
   PROF(7, s, launch_scalar(SC_RHSNORM, B, h->st, h->part, nt, 0.f, 0, s));
   CKL();
   for (int pass = 0; pass < h->opts.max_refine; ++pass) {
+    NvtxRange nv_pass("mpde.refine_pass");
     PROF(7, s, launch_scalar(SC_PASS_BEGIN, B, h->st, h->part, nt, 0.f, 0, s));
     int nact = 0;
     if (int rc = poll_active(h, s, &nact)) return rc;
@@ -1222,6 +1236,7 @@ static uint32_t lz_seed() {
 int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, const float* coeff,
                          void* workspace, size_t workspace_bytes, mpde_stream_t stream_,
                          mpde_hierarchy** out) {
+  NvtxRange nv_api("mpde_build_hierarchy");
   cudaStream_t s = (cudaStream_t)stream_;
   if (int rc = validate(prob, opts)) return rc;
   if (!coeff || !workspace || !out) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
@@ -1375,6 +1390,7 @@ int mpde_destroy_hierarchy(mpde_hierarchy* h) {
 
 int mpde_solve_fwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* bnd, const float* bnd_n,
                       float* z, float* lambda_opt, mpde_stats* stats, mpde_stream_t stream_) {
+  NvtxRange nv_api("mpde_solve_fwd");
   cudaStream_t s = (cudaStream_t)stream_;
   if (!h || !rhs_b || !bnd || !z) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
   const int B = h->B;
@@ -1399,6 +1415,7 @@ int mpde_solve_fwd(mpde_hierarchy* h, const float* rhs_b, const float* bnd, floa
 int mpde_solve_bwd_bc(mpde_hierarchy* h, const float* rhs_b, const float* z, const float* g_z,
                       float* grad_coeff, float* grad_rhs, float* grad_bnd, float* grad_bnd_n,
                       float* dz_opt, mpde_stats* stats, mpde_stream_t stream_) {
+  NvtxRange nv_api("mpde_solve_bwd");
   cudaStream_t s = (cudaStream_t)stream_;
   if (!h || !rhs_b || !z || !g_z || !grad_coeff || !grad_rhs || !grad_bnd)
     return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
@@ -1425,6 +1442,7 @@ int mpde_solve_bwd(mpde_hierarchy* h, const float* rhs_b, const float* z, const 
 }
 
 int mpde_step_gradient(mpde_hierarchy* h, const float* z, float* grad_h, mpde_stream_t stream_) {
+  NvtxRange nv_api("mpde_step_gradient");
   cudaStream_t s = (cudaStream_t)stream_;
   if (!h || !z || !grad_h) return set_err(MPDE_ERR_INVALID_ARG, "null pointer");
   if (!h->lamrows) return set_err(MPDE_ERR_INVALID_ARG, "build with options.grad_steps = 1");
@@ -1445,7 +1463,7 @@ int mpde_apply_normal(const mpde_problem* prob, const float* coeff, const float*
   LevelShape shp[kMaxLevels];
   o.levels_max = 1;
   plan_levels(prob, &o, shp);
-  int scale[kMaxD] = {1, 1, 1};
+  int scale[kMaxD] = {1, 1, 1, 1};
   Geo G = make_geo(prob, shp[0], scale);
   launch_apply_normal(G, prob->batch, coeff, z, q, (cudaStream_t)stream_);
   CKL();
@@ -1481,6 +1499,12 @@ int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* d
   switch (what) {
     case 0: {
       int32_t shp[4] = {lv.G.n[0], lv.G.n[1], h->prob.ndim > 2 ? lv.G.n[2] : 0, h->L};
+      std::memcpy(dst, shp, sizeof(shp));
+      return MPDE_OK;
+    }
+    case 6: {  // host int32[5]: (n0, n1, n2, n3, levels), 0 for dims >= ndim
+      int32_t shp[5] = {0, 0, 0, 0, h->L};
+      for (int d = 0; d < h->prob.ndim; ++d) shp[d] = lv.G.n[d];
       std::memcpy(dst, shp, sizeof(shp));
       return MPDE_OK;
     }
@@ -1619,6 +1643,7 @@ int mpde_fwd_bwd_host(const mpde_problem* prob, const mpde_options* opts, const 
                       float* grad_coeff_h, float* grad_rhs_h, float* grad_bnd_h,
                       void* device_staging, void* workspace, size_t workspace_bytes,
                       mpde_stream_t stream_) {
+  NvtxRange nv_api("mpde_fwd_bwd_host");
   cudaStream_t s = (cudaStream_t)stream_;
   if (int rc = validate(prob, opts)) return rc;
   if (!coeff_h || !rhs_h || !bnd_h || !gz_h || !z_h || !grad_coeff_h || !grad_rhs_h ||

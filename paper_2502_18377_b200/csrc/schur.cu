@@ -1826,8 +1826,11 @@ static inline dim3 grid2(int P, int nvec) { return dim3((P + kThreads - 1) / kTh
     if ((D_) == 2) {         \
       constexpr int DD = 2;  \
       __VA_ARGS__;           \
-    } else {                 \
+    } else if ((D_) == 3) {  \
       constexpr int DD = 3;  \
+      __VA_ARGS__;           \
+    } else {                \
+      constexpr int DD = 4;  \
       __VA_ARGS__;           \
     }                        \
   } while (0)

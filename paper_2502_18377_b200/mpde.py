@@ -226,8 +226,8 @@ def mpde_apply_precond(h, r, z, stream=None):
 
 
 def mpde_hierarchy_query(h, level, what, dst, stream=None):
-    if what in (0, 5):
-        arr = (C.c_int32 * 4)()
+    if what in (0, 5, 6):
+        arr = (C.c_int32 * (5 if what == 6 else 4))()
         _check(lib().mpde_hierarchy_query(h, int(level), int(what), C.cast(arr, C.c_void_p),
                                           _stream(stream)))
         return list(arr)
