@@ -132,6 +132,12 @@ typedef struct {
   int32_t grad_steps; /* 1 = the forward keeps the duals of the derivative and Taylor rows
                          (4*ndim fields per point of workspace) so that mpde_step_gradient
                          can return dl/dh after the backward; default 0        */
+  float   tol_adapt;  /* PCG refinement passes >= 3: a PDE whose error estimate after the
+                         previous pass is e only needs that error shrunk by tol_z / e, so the
+                         pass runs to max(tol_inner2, min(tol_adapt, tol_z / (10 e))) instead
+                         of tol_inner2; its error estimate uses that tolerance.  0 = off;
+                         default 0.1 (C5 forward -14% iterations, C3 -12%, C2 -12%,
+                         DESIGN.md Q14); ignored with krylov = 1                          */
 } mpde_options;
 
 /* one per PDE, device memory, written by mpde_solve_fwd / mpde_solve_bwd */
@@ -145,10 +151,11 @@ typedef struct {
 
 typedef struct mpde_hierarchy mpde_hierarchy; /* opaque, host-side handle */
 
-/* Defaults: tol_z 3e-5 (3.3x below the north_star bar 1e-4; measured errors against the
- * converged oracle references are far below it, Q14; 1e-5 costs a 4th refinement
- * pass on one C4 PDE, profiles/r2_option_sweep.txt), poll_every 4, tol 1e-10, tol_inner 3e-4, tol_inner2 3e-3, max_refine 6, Chebyshev nu = 2, coarsest 8,
- * 16 Lanczos steps, precision 1. */
+/* Defaults: tol_z 1.5e-5 with tol_adapt 0.1 (6.7x below the north_star bar 1e-4; errors
+ * against the converged oracle references and over-converged solves are far below it, and
+ * the adaptive last pass makes the extra margin cheap: DESIGN.md Q14,
+ * profiles/r2_stop_rule.txt), poll_every 4, tol 1e-10, tol_inner 3e-4, tol_inner2 3e-3,
+ * max_refine 6, Chebyshev nu = 2, coarsest 8, 16 Lanczos steps, precision 1. */
 mpde_options mpde_default_options(void);
 
 /* n_v = |M| * P variables, n_c constraint rows (Eqs. 3-7 counted), levels of the

@@ -74,6 +74,8 @@ struct PdeState {
   float tol;       // residual floor (stop when ||A^T(d-Az)||/||A^T d|| <= tol)
   float tol_z;     // error-based stop (estimated ||z - z*|| / ||z|| <= tol_z)
   float tol2_later;  // (PCG relative tolerance of refinement passes >= 2)^2
+  double* tolp;      // [B] squared relative tolerance of the current pass (passes >= 2)
+  float adapt_max;   // passes >= 3: options.tol_adapt (0: off; Q14)
 };
 
 // FGMRES(m) (fgmres.cu, opts.krylov = 1): per-PDE Arnoldi state, arrays over the batch

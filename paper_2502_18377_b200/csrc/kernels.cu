@@ -756,6 +756,19 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
     st.inpass[v] = st.done[v] ? 0 : 1;
     st.act[v] = st.inpass[v];
     if (st.inpass[v]) st.refines[v] += 1;
+    {
+      // pass k+1 >= 3 must shrink the error by tol_z / err_k (with a 10x margin), not by
+      // tol_inner2: the relative tolerance tau = tol_z / (10 err_k), clamped to
+      // [tol_inner2, adapt_max]; the error estimate of the pass then uses tau (SC_CORR)
+      double t2 = (double)st.tol2_later;
+      if (st.adapt_max > 0.f && st.refines[v] >= 3 && st.errest[v] > 0.0) {
+        double tau = (double)st.tol_z / (10.0 * st.errest[v]);
+        tau = fmin(tau, (double)st.adapt_max);
+        tau = fmax(tau, sqrt((double)st.tol2_later));
+        t2 = tau * tau;
+      }
+      st.tolp[v] = t2;
+    }
     st.pass_iters[v] = 0;
     st.failed[v] = 0;
     return;
@@ -793,7 +806,7 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
     // geometric refinement: err_k ~ ||d_k|| * rho_k with rho_k the larger of the observed
     // contraction ||d_k|| / ||d_{k-1}|| and the relative tolerance pass k was solved to
     const double est = st.refines[v] >= 2 && st.dzprev[v] > 0
-                           ? dz * fmax(dz / st.dzprev[v], sqrt((double)st.tol2_later))
+                           ? dz * fmax(dz / st.dzprev[v], sqrt(st.tolp[v]))
                            : dz;
     st.dzprev[v] = dz;
     st.errest[v] = zn > 0 ? est / zn : (dz > 0 ? 1.0 : 0.0);
@@ -879,7 +892,7 @@ __global__ void k_scalar(int op, int B, PdeState st, const double* part, int nt,
     st.pass_iters[v] += 1;
     if (!isfinite(rr)) {
       pcg_fail(st, v, rr);
-    } else if (rr <= (st.refines[v] >= 2 ? (double)st.tol2_later : (double)tol2) * st.rr0[v] ||
+    } else if (rr <= (st.refines[v] >= 2 ? st.tolp[v] : (double)tol2) * st.rr0[v] ||
                st.pass_iters[v] >= max_iters ||
                rr <= 0.25 * (double)st.tol * st.tol * st.rhsn[v] * st.rhsn[v]) {
       // pass finished: relative inner tolerance (the fp32 limit) reached, or the outer

@@ -110,6 +110,8 @@ int validate(const mpde_problem* pr, const mpde_options* op) {
     return set_err(MPDE_ERR_INVALID_ARG, "lanczos_steps must be in 2..32");
   if (op->precision < 0 || op->precision > 3)
     return set_err(MPDE_ERR_INVALID_ARG, "precision must be in 0..3");
+  if (!(op->tol_adapt >= 0.f && op->tol_adapt < 1.f))
+    return set_err(MPDE_ERR_INVALID_ARG, "tol_adapt must be in [0, 1)");
   if (op->grad_steps != 0 && op->grad_steps != 1)
     return set_err(MPDE_ERR_INVALID_ARG, "grad_steps must be 0 or 1");
   if (!(op->tol > 0) || !(op->tol_inner > 0) || !(op->tol_z > 0) || !(op->tol_inner2 > 0))
@@ -487,6 +489,7 @@ size_t plan_workspace(const mpde_problem* pr, const mpde_options* op, char* base
   h->st.failed = bp.take<int>(B);
   h->st.dzprev = bp.take<double>(B);
   h->st.errest = bp.take<double>(B);
+  h->st.tolp = bp.take<double>(B);
   h->d_count = bp.take<int>(2);
   if (op->grad_steps) {
     h->lamrows = bp.take<float>((size_t)B * 4 * D * P);
@@ -835,6 +838,7 @@ static std::string graph_key(const mpde_hierarchy* h, int k, int device) {
   key_put(key, o.precision);
   key_put(key, o.use_graphs);
   key_put(key, o.tol_z);
+  key_put(key, o.tol_adapt);
   key_put(key, o.tol_inner2);
   key_put(key, o.cf_bf16);
   key_put(key, o.krylov);
@@ -1170,7 +1174,8 @@ extern "C" {
 mpde_options mpde_default_options(void) {
   mpde_options o;
   o.tol = 1e-10f;
-  o.tol_z = 3e-5f;  // 3.3x below the north_star z tolerance (Q14: stop margin)
+  o.tol_z = 1.5e-5f;  // 6.7x below the north_star z tolerance (Q14: stop margin)
+  o.tol_adapt = 0.1f;  // passes >= 3 solve only as far as the error estimate requires
   o.tol_inner = 3e-4f;
   o.max_iters = 500;
   o.max_refine = 6;
@@ -1284,6 +1289,7 @@ int mpde_build_hierarchy(const mpde_problem* prob, const mpde_options* opts, con
     // krylov = 1 every pass runs to min(tol_inner, tol_inner2) (C2 e_z 2.9e-5; Q14)
     const float t2 = opts->krylov == 1 ? std::min(opts->tol_inner, opts->tol_inner2) : opts->tol_inner2;
     h->st.tol2_later = t2 * t2;
+    h->st.adapt_max = opts->krylov == 0 ? opts->tol_adapt : 0.f;
   }
   const int B = h->B, M = h->M, L = h->L;
   g_launch_count += 2;

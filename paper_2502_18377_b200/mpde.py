@@ -38,7 +38,7 @@ class mpde_options(C.Structure):
                 ("lanczos_steps", C.c_int32), ("precision", C.c_int32),
                 ("use_graphs", C.c_int32), ("tol_z", C.c_float), ("tol_inner2", C.c_float),
                 ("cf_bf16", C.c_int32), ("krylov", C.c_int32), ("restart", C.c_int32),
-                ("grad_steps", C.c_int32)]
+                ("grad_steps", C.c_int32), ("tol_adapt", C.c_float)]
 
 
 class mpde_stats(C.Structure):

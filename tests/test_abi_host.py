@@ -29,7 +29,8 @@ def test_exports_every_declared_symbol(mp):
     assert declared == set(mp.EXPORTS)
 
 
-@pytest.mark.parametrize("shape", [(16, 16), (32, 32), (101, 256), (32, 32, 32), (32, 64, 64)])
+@pytest.mark.parametrize("shape", [(16, 16), (32, 32), (101, 256), (32, 32, 32), (32, 64, 64), (6, 7, 6, 8),
+                                   (12, 16, 16, 20)])
 def test_sizes_match_oracle_counts(mp, shape):
     prob = mp.make_problem(shape, [0.1] * len(shape), 4)
     n_v, n_c, _ = mp.mpde_sizes(prob)
@@ -106,3 +107,21 @@ def test_fgmres_options_and_workspace(mp):
     lib = mp.lib()
     for kw in ({"krylov": 1, "restart": 0}, {"krylov": 1, "restart": 33}, {"krylov": 2}):
         assert lib.mpde_workspace_bytes(C.byref(pr), C.byref(mp.mpde_default_options(**kw))) == 0
+
+
+def test_adaptive_pass_tolerance_option(mp):
+    """options.tol_adapt (Q14): default 0.1, 0 disables, values outside [0, 1)
+    are rejected (workspace 0); ndim 4 is accepted and ndim 5 rejected."""
+    import ctypes as C
+    lib = mp.lib()
+    assert abs(mp.mpde_default_options().tol_adapt - 0.1) < 1e-7
+    pr = mp.make_problem((16, 16), (0.1, 0.1), 1)
+    assert mp.mpde_workspace_bytes(pr, mp.mpde_default_options(tol_adapt=0.0)) > 0
+    for bad in (-0.1, 1.0, float("nan")):
+        assert lib.mpde_workspace_bytes(C.byref(pr), C.byref(mp.mpde_default_options(tol_adapt=bad))) == 0
+    p4 = mp.make_problem((6, 7, 6, 8), (0.1,) * 4, 2)
+    n_v, n_c, L = mp.mpde_sizes(p4)
+    assert n_v == 9 * 6 * 7 * 6 * 8 and L == 1
+    p5 = mp.make_problem((6, 6, 6, 6), (0.1,) * 4, 1)
+    p5.ndim = 5
+    assert lib.mpde_sizes(C.byref(p5), None, None, None, None) == 2
