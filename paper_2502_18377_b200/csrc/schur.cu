@@ -16,6 +16,7 @@
 // Per point the kernels read cf = [sigma alpha, 1/sigma, u~ (2D)] (2+2D floats).
 #include "common.cuh"
 #include <cuda_bf16.h>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -372,6 +373,29 @@ __device__ __forceinline__ void stT4(T* p, const T* v) {
   }
 }
 #define F4(a, j) (j == 0 ? a.x : (j == 1 ? a.y : (j == 2 ? a.z : a.w)))
+// Quad updates a[0..3] (+)= ... either as four scalar ops or on the packed fp32x2 pipe
+// (FFMA2 / FMUL2 on sm_100a: half the issue slots; each lane is the same single-rounding
+// op, so both forms give bit-identical results).  Measured (profiles/r2_ffma2_ab.txt): pass 1
+// gains (0.420 -> 0.428 of the HBM peak), pass 2 does not (74.3 -> 75.0 us per level-0
+// launch: it waits on L1 wavefronts, not on issue), so pass 2 keeps the scalar form.
+// acc[0..3] += c * v
+template <bool PACKED>
+__device__ __forceinline__ void quad_axpy(float* acc, float c, const float4& v) {
+  if constexpr (PACKED) {
+    const float2 cc = make_float2(c, c);
+    const float2 lo = __ffma2_rn(cc, make_float2(v.x, v.y), make_float2(acc[0], acc[1]));
+    const float2 hi = __ffma2_rn(cc, make_float2(v.z, v.w), make_float2(acc[2], acc[3]));
+    acc[0] = lo.x; acc[1] = lo.y; acc[2] = hi.x; acc[3] = hi.y;
+  } else {
+    acc[0] += c * v.x; acc[1] += c * v.y; acc[2] += c * v.z; acc[3] += c * v.w;
+  }
+}
+// acc[0..3] -= (a * va + b * vb) * hv   (the K^T (u~ h) terms)
+__device__ __forceinline__ void quad_kt(float* acc, float a, float b, const float4& va, const float4& vb,
+                                        const float4& hv) {
+  acc[0] -= (a * va.x + b * vb.x) * hv.x; acc[1] -= (a * va.y + b * vb.y) * hv.y;
+  acc[2] -= (a * va.z + b * vb.z) * hv.z; acc[3] -= (a * va.w + b * vb.w) * hv.w;
+}
 // NV 16-byte loads of a table-row segment (rows and segments are 16-byte aligned): one
 // vector load per 4 coefficients instead of one scalar load each (L1 wavefronts)
 template <int NV>
@@ -435,11 +459,16 @@ __device__ __forceinline__ void schur_h4(const Geo& G, const CF* __restrict__ cb
 #pragma unroll
       for (int o = -2; o <= 2; ++o) {
         const float4 xv = ld4(xb + p0 + o * s);
-        const T a = G.irow[d][(o + 2) * 2], b = G.irow[d][(o + 2) * 2 + 1];
+        if constexpr (std::is_same<T, float>::value) {
+          quad_axpy<true>(k1, G.irow[d][(o + 2) * 2], xv);
+          quad_axpy<true>(k2, G.irow[d][(o + 2) * 2 + 1], xv);
+        } else {
+          const T a = G.irow[d][(o + 2) * 2], b = G.irow[d][(o + 2) * 2 + 1];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          k1[j] += a * T(F4(xv, j));
-          k2[j] += b * T(F4(xv, j));
+          for (int j = 0; j < 4; ++j) {
+            k1[j] += a * T(F4(xv, j));
+            k2[j] += b * T(F4(xv, j));
+          }
         }
       }
     } else {  // edge rows: unrolled, clamped addresses, zero coefficients out of range
@@ -793,29 +822,15 @@ __device__ __forceinline__ void pencil2(const Geo& G, const CF* __restrict__ cb,
 #pragma unroll
     for (int u = -4; u <= 5; ++u) {
       const float4 xv = ld4(xb + pbase + u * s);
-      const float c0 = u <= 4 ? G.irow[AX][20 + u + 4] : 0.f;
-      const float c1 = u >= -3 ? G.irow[AX][20 + u - 1 + 4] : 0.f;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        acc0[j] += c0 * F4(xv, j);
-        acc1[j] += c1 * F4(xv, j);
-      }
+      if (u <= 4) quad_axpy<false>(acc0, G.irow[AX][20 + u + 4], xv);
+      if (u >= -3) quad_axpy<false>(acc1, G.irow[AX][20 + u - 1 + 4], xv);
     }
 #pragma unroll
     for (int u = -2; u <= 3; ++u) {
       const int q = pbase + u * s;
       const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q), hv = ld4(hb + q);
-      const float a0 = u <= 2 ? G.irow[AX][10 + (u + 2) * 2] : 0.f;
-      const float b0 = u <= 2 ? G.irow[AX][10 + (u + 2) * 2 + 1] : 0.f;
-      const float a1 = u >= -1 ? G.irow[AX][10 + (u + 1) * 2] : 0.f;
-      const float b1 = u >= -1 ? G.irow[AX][10 + (u + 1) * 2 + 1] : 0.f;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float w0 = (a0 * F4(va, j) + b0 * F4(vb, j)) * F4(hv, j);
-        const float w1 = (a1 * F4(va, j) + b1 * F4(vb, j)) * F4(hv, j);
-        acc0[j] -= w0;
-        acc1[j] -= w1;
-      }
+      if (u <= 2) quad_kt(acc0, G.irow[AX][10 + (u + 2) * 2], G.irow[AX][10 + (u + 2) * 2 + 1], va, vb, hv);
+      if (u >= -1) quad_kt(acc1, G.irow[AX][10 + (u + 1) * 2], G.irow[AX][10 + (u + 1) * 2 + 1], va, vb, hv);
     }
     return;
   }
@@ -830,13 +845,8 @@ __device__ __forceinline__ void pencil2(const Geo& G, const CF* __restrict__ cb,
   for (int u = -5; u <= 6; ++u) {
     const int ic = min(max(i0 + u, 0), n - 1);
     const float4 xv = ld4(xb + pbase + (ic - i0) * s);
-    const float c0 = u <= 5 ? p0a[u + 5] : 0.f;
-    const float c1 = u >= -4 ? m1 * p0b[u - 1 + 5] : 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      acc0[j] += c0 * F4(xv, j);
-      acc1[j] += c1 * F4(xv, j);
-    }
+    if (u <= 5) quad_axpy<false>(acc0, p0a[u + 5], xv);
+    if (u >= -4) quad_axpy<false>(acc1, m1 * p0b[u - 1 + 5], xv);
   }
   float kta[20], ktb[20];
   ldv<5>(r0 + kTabKT, kta);
@@ -846,15 +856,8 @@ __device__ __forceinline__ void pencil2(const Geo& G, const CF* __restrict__ cb,
     const int ic = min(max(i0 + u, 0), n - 1);
     const int q = pbase + (ic - i0) * s;
     const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q), hv = ld4(hb + q);
-    const float a0 = u <= 4 ? kta[(u + 4) * 2] : 0.f;
-    const float b0 = u <= 4 ? kta[(u + 4) * 2 + 1] : 0.f;
-    const float a1 = u >= -3 ? m1 * ktb[(u + 3) * 2] : 0.f;
-    const float b1 = u >= -3 ? m1 * ktb[(u + 3) * 2 + 1] : 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      acc0[j] -= (a0 * F4(va, j) + b0 * F4(vb, j)) * F4(hv, j);
-      acc1[j] -= (a1 * F4(va, j) + b1 * F4(vb, j)) * F4(hv, j);
-    }
+    if (u <= 4) quad_kt(acc0, kta[(u + 4) * 2], kta[(u + 4) * 2 + 1], va, vb, hv);
+    if (u >= -3) quad_kt(acc1, m1 * ktb[(u + 3) * 2], m1 * ktb[(u + 3) * 2 + 1], va, vb, hv);
   }
 }
 
@@ -870,17 +873,13 @@ __device__ __forceinline__ void pencil1(const Geo& G, const CF* __restrict__ cb,
 #pragma unroll
     for (int o = -4; o <= 4; ++o) {
       const float4 xv = ld4(xb + p0 + o * s);
-      const float a = G.irow[AX][20 + o + 4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[j] += a * F4(xv, j);
+      quad_axpy<false>(acc, G.irow[AX][20 + o + 4], xv);
     }
 #pragma unroll
     for (int o = -2; o <= 2; ++o) {
       const int q = p0 + o * s;
       const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q), hv = ld4(hb + q);
-      const float a = G.irow[AX][10 + (o + 2) * 2], b = G.irow[AX][10 + (o + 2) * 2 + 1];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[j] -= (a * F4(va, j) + b * F4(vb, j)) * F4(hv, j);
+      quad_kt(acc, G.irow[AX][10 + (o + 2) * 2], G.irow[AX][10 + (o + 2) * 2 + 1], va, vb, hv);
     }
     return;
   }
@@ -893,18 +892,14 @@ __device__ __forceinline__ void pencil1(const Geo& G, const CF* __restrict__ cb,
   for (int o = -5; o <= 5; ++o) {
     const int oc = o < olo ? olo : (o > ohi ? ohi : o);
     const float4 xv = ld4(xb + p0 + oc * s);
-    const float a = p0r[o + 5];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] += a * F4(xv, j);
+    quad_axpy<false>(acc, p0r[o + 5], xv);
   }
 #pragma unroll
   for (int o = -4; o <= 4; ++o) {
     const int oc = o < olo ? olo : (o > ohi ? ohi : o);
     const int q = p0 + oc * s;
     const float4 va = ldc4(u1 + q), vb = ldc4(u2 + q), hv = ld4(hb + q);
-    const float a = ktr[(o + 4) * 2], b = ktr[(o + 4) * 2 + 1];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] -= (a * F4(va, j) + b * F4(vb, j)) * F4(hv, j);
+    quad_kt(acc, ktr[(o + 4) * 2], ktr[(o + 4) * 2 + 1], va, vb, hv);
   }
 }
 
