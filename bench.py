@@ -36,7 +36,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
-METRIC = "PDE solves/s (fwd+bwd) at 64^2x32 grid, batch 32; HBM GB/s vs peak"
+
+def _baseline_metric():
+    """BASELINE.json's metric string, verbatim (the driver matches the line against it)."""
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f)["metric"]
+    except (OSError, KeyError, ValueError):
+        return "PDE solves/s (fwd+bwd) at 64\u00b2\u00d732 grid, batch 32; HBM GB/s vs peak"
+
+
+METRIC = _baseline_metric()
 UNIT = "PDE solves/s (fwd+bwd)"
 # algorithmic bytes per point of S pass 2 (k_schur_s_*), per epilogue kind: x 4 + h 4 +
 # cf[7] 28 (sigma alpha, u~ 2D) read + the epilogue's vector traffic (DESIGN.md §4)

@@ -1858,9 +1858,14 @@ static inline bool small_level(const Geo& G) {
 }
 static inline int v4_threads(const Geo& G) { return small_level(G) ? kSmallThreads : kThreads; }
 // warp-specialised interior / edge quads (remap_quad): NY4 a power of two dividing kThreads
+static int g_remap = -1;  // env MPDE_REMAP=1: warp-specialised interior / edge quad mapping
 static inline int use_remap(const Geo& G) {
+  if (g_remap < 0) {
+    const char* e = getenv("MPDE_REMAP");
+    g_remap = e ? atoi(e) : 0;  // default natural: see DESIGN.md §4 tuning table
+  }
   const int q = G.n[G.D - 1] >> 2;
-  return use_v4(G) && !small_level(G) && q > 0 && (q & (q - 1)) == 0 && q <= kThreads;
+  return g_remap && use_v4(G) && !small_level(G) && q > 0 && (q & (q - 1)) == 0 && q <= kThreads;
 }
 // 2x2 (t,x)-blocked pass 2: 3D, fp32, n_y % 4 == 0
 static int g_block_mode = -1;  // 0: v4, 1: 2x1 (t), 2: 2x2 (t,x); env MPDE_SCHUR_BLOCK

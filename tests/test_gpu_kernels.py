@@ -99,13 +99,14 @@ _MARCH = {"MPDE_MARCH": "2"}  # the march on every eligible level, whatever the 
     ((8, 16, 16), (0.05, 0.06, 0.07), {"MPDE_SLAB": "1"}, (11, 11), 3),         # C4 level-2 geometry: 2-CTA t-slab clusters
     ((7, 16, 32), (0.05, 0.06, 0.07), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7), 2),  # fused, 2 x-tiles
     ((9, 24, 36), (0.04, 0.03, 0.05), {"MPDE_FUSED": "1", **_NOSMALL}, (7, 7), 2),  # fused, interior tile
-    ((7, 16, 64), (0.05, 0.06, 0.07), _NOSMALL, (1, 3), 2),      # t-blocked, warp-specialised y (NY4=16)
-    ((8, 10, 32), (0.05, 0.06, 0.07), _NOSMALL, (1, 3), 2),      # t-blocked, NY4=8 (4 interior / 4 edge)
-    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_HY": "1", **_NOSMALL}, (8, 3), 2),  # y part in pass 1
-    ((9, 12, 32), (0.05, 0.06, 0.07), {"MPDE_HY": "1", **_NOSMALL}, (8, 3), 2),
+    ((7, 16, 64), (0.05, 0.06, 0.07), _NOSMALL, (1, 3), 2),      # t-blocked, natural quad mapping (NY4=16)
+    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_REMAP": "1", **_NOSMALL}, (1, 3), 2),  # warp-specialised y quads
+    ((8, 10, 32), (0.05, 0.06, 0.07), {"MPDE_REMAP": "1", **_NOSMALL}, (1, 3), 2),  # NY4=8 (4 interior / 4 edge)
+    ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_HY": "1", "MPDE_REMAP": "1", **_NOSMALL}, (8, 3), 2),  # y part in pass 1
+    ((9, 12, 32), (0.05, 0.06, 0.07), {"MPDE_HY": "1", "MPDE_REMAP": "1", **_NOSMALL}, (8, 3), 2),
     ((7, 16, 64), (0.05, 0.06, 0.07), {"MPDE_TILE": "1", **_NOSMALL}, (1, 6), 2),   # smem-tiled pass 2
     ((13, 12, 32), (0.05, 0.06, 0.07), {"MPDE_TILE": "1", **_NOSMALL}, (1, 6), 2),  # partial last t tile
-    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_B22_TP": "4", **_NOSMALL}, (1, 3), 2),  # t-pair CTA tiling
+    ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_B22_TP": "4", "MPDE_REMAP": "1", **_NOSMALL}, (1, 3), 2),  # t-pair CTA tiling
     ((9, 16, 64), (0.05, 0.06, 0.07), {"MPDE_SCHUR_BLOCK": "2", **_NOSMALL}, (1, 5), 2)])  # 2x2 blocking
 def test_large_schur_matches_sparse(shape, h, env, kinds, B, tmp_path):
     """S apply through every 3D kernel variant, incl. the production instantiations the
