@@ -17,6 +17,11 @@
 #include "common.cuh"
 #include <cuda_bf16.h>
 #include <type_traits>
+// A/B build switch: MPDE_B22_MINB = pass-2 CTAs per SM the register allocation targets
+// (3: 80 registers; 4 = 64 registers measured slower, profiles/r2_b22_regs_ab.txt)
+#ifndef MPDE_B22_MINB
+#define MPDE_B22_MINB 3
+#endif
 
 #include "internal.h"
 
@@ -922,51 +927,65 @@ __device__ __forceinline__ void quad_y_own(const Geo& G, const CF* __restrict__ 
   }
   const CF* u1 = cb + (size_t)6 * P;
   const CF* u2 = cb + (size_t)7 * P;
-  float xw[20], aw[12], bw[12], hw[12];
+  // x window first (P0 taps), then the u~ h windows (K^T taps): fewer values live at once
+  // (pass-2 spill 40 -> 8 B, 71.3 -> 69.1 us per level-0 launch; profiles/r2_b22_regs_ab.txt)
+  {
+    float xw[20];
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const int off = -8 + 4 * k;
-    const bool ok = (i0 + off >= 0) && (i0 + off < n);
-    const float4 vv = ok ? ld4(xb + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < 5; ++k) {
+      const int off = -8 + 4 * k;
+      const bool ok = (i0 + off >= 0) && (i0 + off < n);
+      const float4 vv = ok ? ld4(xb + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) xw[4 * k + j] = F4(vv, j);
-  }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const int off = -4 + 4 * k;
-    const bool ok = (i0 + off >= 0) && (i0 + off < n);
-    const float4 va = ok ? ldc4(u1 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 vb = ok ? ldc4(u2 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 hv = ok ? ld4(hb + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < 4; ++j) xw[4 * k + j] = F4(vv, j);
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      aw[4 * k + j] = F4(va, j);
-      bw[4 * k + j] = F4(vb, j);
-      hw[4 * k + j] = F4(hv, j);
+      const int i = i0 + j;
+      if (ymode == 1 || (ymode == 0 && i >= 7 && i <= n - 8)) {
+#pragma unroll
+        for (int o = -4; o <= 4; ++o) acc[j] += G.irow[2][20 + o + 4] * xw[8 + j + o];
+      } else {
+        float p0r[12];
+        ldv<3>(tab_row(G, 2, i) + kTabP0, p0r);
+#pragma unroll
+        for (int o = -5; o <= 5; ++o) acc[j] += p0r[o + 5] * xw[8 + j + o];
+      }
     }
   }
+  {
+    float aw[12], bw[12], hw[12];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int i = i0 + j;
-    if (ymode == 1 || (ymode == 0 && i >= 7 && i <= n - 8)) {
+    for (int k = 0; k < 3; ++k) {
+      const int off = -4 + 4 * k;
+      const bool ok = (i0 + off >= 0) && (i0 + off < n);
+      const float4 va = ok ? ldc4(u1 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 vb = ok ? ldc4(u2 + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 hv = ok ? ld4(hb + p0 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int o = -4; o <= 4; ++o) acc[j] += G.irow[2][20 + o + 4] * xw[8 + j + o];
+      for (int j = 0; j < 4; ++j) {
+        aw[4 * k + j] = F4(va, j);
+        bw[4 * k + j] = F4(vb, j);
+        hw[4 * k + j] = F4(hv, j);
+      }
+    }
 #pragma unroll
-      for (int o = -2; o <= 2; ++o)
-        acc[j] -= (G.irow[2][10 + (o + 2) * 2] * aw[4 + j + o] +
-                   G.irow[2][10 + (o + 2) * 2 + 1] * bw[4 + j + o]) * hw[4 + j + o];
-    } else {
-      const float* row = tab_row(G, 2, i);
-      float p0r[12], ktr[20];
-      ldv<3>(row + kTabP0, p0r);
-      ldv<5>(row + kTabKT, ktr);
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j;
+      if (ymode == 1 || (ymode == 0 && i >= 7 && i <= n - 8)) {
 #pragma unroll
-      for (int o = -5; o <= 5; ++o) acc[j] += p0r[o + 5] * xw[8 + j + o];
+        for (int o = -2; o <= 2; ++o)
+          acc[j] -= (G.irow[2][10 + (o + 2) * 2] * aw[4 + j + o] +
+                     G.irow[2][10 + (o + 2) * 2 + 1] * bw[4 + j + o]) * hw[4 + j + o];
+      } else {
+        float ktr[20];
+        ldv<5>(tab_row(G, 2, i) + kTabKT, ktr);
 #pragma unroll
-      for (int o = -4; o <= 4; ++o) {
-        if (4 + j + o < 0 || 4 + j + o > 11) continue;
-        acc[j] -= (ktr[(o + 4) * 2] * aw[4 + j + o] +
-                   ktr[(o + 4) * 2 + 1] * bw[4 + j + o]) * hw[4 + j + o];
+        for (int o = -4; o <= 4; ++o) {
+          if (4 + j + o < 0 || 4 + j + o > 11) continue;
+          acc[j] -= (ktr[(o + 4) * 2] * aw[4 + j + o] +
+                     ktr[(o + 4) * 2 + 1] * bw[4 + j + o]) * hw[4 + j + o];
+        }
       }
     }
   }
@@ -1042,7 +1061,7 @@ __device__ __forceinline__ double quad_epilogue(const EpiArgs& A, int pde, size_
 }
 
 template <int EPI, int BX, int NX, int NY, int YP, typename CF = float>
-__global__ void __launch_bounds__(kThreads, 3) k_schur_s_b22(Geo G, const CF* __restrict__ cf, int crep,
+__global__ void __launch_bounds__(kThreads, MPDE_B22_MINB) k_schur_s_b22(Geo G, const CF* __restrict__ cf, int crep,
                                                          const float* __restrict__ x,
                                                          const float* __restrict__ hb, EpiArgs A,
                                                          const int* act, int remap) {
