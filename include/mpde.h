@@ -264,7 +264,10 @@ int mpde_hierarchy_query(mpde_hierarchy* h, int32_t level, int32_t what, void* d
 /* Host-buffer end-to-end call: copies the inputs from HOST memory (pinned for
  * asynchrony) into `device_staging` (>= mpde_host_staging_bytes), builds the
  * hierarchy in `workspace`, runs forward + backward with g_z, and copies z, grad_coeff,
- * grad_rhs, grad_bnd back to HOST memory.  Synchronises `stream` before returning. */
+ * grad_rhs, grad_bnd back to HOST memory.  Synchronises `stream` before returning.
+ * The H2D of g_z overlaps the build and the forward, and the D2H of z the backward, on a
+ * per-thread side stream of the library that is joined back into `stream` (events recorded
+ * on `stream` around the call cover every copy). */
 size_t mpde_host_staging_bytes(const mpde_problem* prob);
 int mpde_fwd_bwd_host(const mpde_problem* prob, const mpde_options* opts,
                       const float* coeff_h, const float* rhs_h, const float* bnd_h,

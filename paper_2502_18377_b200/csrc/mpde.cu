@@ -1667,18 +1667,53 @@ int mpde_fwd_bwd_host(const mpde_problem* prob, const mpde_options* opts, const 
   float* om = bp.take<float>(B * P);
   float* gb = bp.take<float>(B * P);
   float* gw = bp.take<float>(B * P);
+  // A per-thread side stream overlaps the two largest copies with compute: the H2D of g_z with
+  // the build and the forward, the D2H of z* with the backward (each |M| fields, 117 MB at C4)
+  struct CopyRes {
+    int dev = -1;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  };
+  static thread_local CopyRes cr;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (cr.dev != dev) {
+    CK(cudaStreamCreateWithFlags(&cr.cs, cudaStreamNonBlocking));
+    for (auto& e : cr.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cr.dev = dev;
+  }
+  cudaStream_t cs = cr.cs;
   CK(cudaMemcpyAsync(c, coeff_h, sizeof(float) * B * M * P, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(b, rhs_h, sizeof(float) * B * P, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(om, bnd_h, sizeof(float) * B * P, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(g, gz_h, sizeof(float) * B * M * P, cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(cr.ev[0], s));  // g_z queues behind c, b, omega on the H2D link
+  CK(cudaStreamWaitEvent(cs, cr.ev[0], 0));
+  CK(cudaMemcpyAsync(g, gz_h, sizeof(float) * B * M * P, cudaMemcpyHostToDevice, cs));
+  CK(cudaEventRecord(cr.ev[1], cs));
+  auto join = [&]() {  // the caller's stream (and its timing events) cover the side stream
+    cudaEventRecord(cr.ev[3], cs);
+    cudaStreamWaitEvent(s, cr.ev[3], 0);
+  };
   mpde_hierarchy* h = nullptr;
-  if (int rc = mpde_build_hierarchy(prob, opts, c, workspace, workspace_bytes, stream_, &h))
+  if (int rc = mpde_build_hierarchy(prob, opts, c, workspace, workspace_bytes, stream_, &h)) {
+    join();
+    cudaStreamSynchronize(s);
     return rc;
+  }
   int rc = mpde_solve_fwd(h, b, om, z, nullptr, stream_);
-  if (!rc) rc = mpde_solve_bwd(h, b, z, g, gc, gb, gw, nullptr, nullptr, stream_);
+  if (!rc) {
+    CK(cudaEventRecord(cr.ev[2], s));  // z* final: copy it out while the backward runs
+    CK(cudaStreamWaitEvent(cs, cr.ev[2], 0));
+    CK(cudaMemcpyAsync(z_h, z, sizeof(float) * B * M * P, cudaMemcpyDeviceToHost, cs));
+    CK(cudaStreamWaitEvent(s, cr.ev[1], 0));
+    rc = mpde_solve_bwd(h, b, z, g, gc, gb, gw, nullptr, nullptr, stream_);
+  }
   mpde_destroy_hierarchy(h);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(z_h, z, sizeof(float) * B * M * P, cudaMemcpyDeviceToHost, s));
+  join();
+  if (rc) {
+    cudaStreamSynchronize(s);
+    return rc;
+  }
   CK(cudaMemcpyAsync(grad_coeff_h, gc, sizeof(float) * B * M * P, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(grad_rhs_h, gb, sizeof(float) * B * P, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(grad_bnd_h, gw, sizeof(float) * B * P, cudaMemcpyDeviceToHost, s));
