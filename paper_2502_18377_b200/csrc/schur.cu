@@ -19,6 +19,7 @@
 #include <type_traits>
 // A/B build switch: MPDE_B22_MINB = pass-2 CTAs per SM the register allocation targets
 // (3: 80 registers; 4 = 64 registers measured slower, profiles/r2_b22_regs_ab.txt)
+constexpr int kSmallThreads = 64;  // CTA size of the small-level (<= MPDE_SMALLP points) kernels
 #ifndef MPDE_B22_MINB
 #define MPDE_B22_MINB 3
 #endif
@@ -672,6 +673,125 @@ __device__ __forceinline__ void schur_s4(const Geo& G, const CF* __restrict__ cb
       }
     }
   }
+}
+
+// Small-level form of schur_h4 (latency bound: ~2 warps per SM): every x tap of the t / x
+// stencils (9, clamped) and every coefficient is loaded before any edge-class branch, so
+// the thread pays one memory round trip instead of one per axis.  Interior rows use taps
+// -2..2 with irow, edge rows the table (-4..4), in the same order as schur_h4: bit-identical.
+template <int D, typename T, typename CF>
+__device__ __forceinline__ void schur_h4_lat(const Geo& G, const CF* __restrict__ cb,
+                                             const float* __restrict__ xb, int p0, const int* idx,
+                                             T* g) {
+  const int P = G.P;
+  float4 xt[D - 1][9];
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) {
+    const int n = G.n[d], s = G.stride[d], i = idx[d];
+#pragma unroll
+    for (int o = -4; o <= 4; ++o) {
+      const int oc = min(max(i + o, 0), n - 1) - i;
+      xt[d][o + 4] = ld4(xb + p0 + oc * s);
+    }
+  }
+  float4 ua[D], ub[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    ua[d] = ldc4(cb + (size_t)(2 + 2 * d) * P + p0);
+    ub[d] = ldc4(cb + (size_t)(3 + 2 * d) * P + p0);
+  }
+  constexpr int dl = D - 1;
+  const int nl = G.n[dl], i0 = idx[dl];
+  const float4 wl = i0 >= 4 ? ld4(xb + p0 - 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 wm = ld4(xb + p0);
+  const float4 wr = i0 + 4 < nl ? ld4(xb + p0 + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 c0 = ldc4(cb + p0), c1 = ldc4(cb + P + p0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) g[j] = T(F4(c0, j)) * T(F4(wm, j));
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) {
+    const int n = G.n[d], i = idx[d];
+    T k1[4] = {0, 0, 0, 0}, k2[4] = {0, 0, 0, 0};
+    if (i >= 2 && i <= n - 3) {
+#pragma unroll
+      for (int o = -2; o <= 2; ++o) {
+        const T a = G.irow[d][(o + 2) * 2], b = G.irow[d][(o + 2) * 2 + 1];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          k1[j] += a * T(F4(xt[d][o + 4], j));
+          k2[j] += b * T(F4(xt[d][o + 4], j));
+        }
+      }
+    } else {
+      float kf[20];
+      ldv<5>(tab_row(G, d, i) + kTabKf, kf);
+#pragma unroll
+      for (int o = -4; o <= 4; ++o) {
+        const T a = kf[(o + 4) * 2], b = kf[(o + 4) * 2 + 1];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          k1[j] += a * T(F4(xt[d][o + 4], j));
+          k2[j] += b * T(F4(xt[d][o + 4], j));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g[j] -= T(F4(ua[d], j)) * k1[j] + T(F4(ub[d], j)) * k2[j];
+  }
+  {
+    float w[12];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      w[j] = F4(wl, j);
+      w[4 + j] = F4(wm, j);
+      w[8 + j] = F4(wr, j);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j;
+      T k1 = 0, k2 = 0;
+      if (i >= 2 && i <= nl - 3) {
+#pragma unroll
+        for (int o = -2; o <= 2; ++o) {
+          k1 += T(G.irow[dl][(o + 2) * 2]) * T(w[4 + j + o]);
+          k2 += T(G.irow[dl][(o + 2) * 2 + 1]) * T(w[4 + j + o]);
+        }
+      } else {
+        float kf[20];
+        ldv<5>(tab_row(G, dl, i) + kTabKf, kf);
+#pragma unroll
+        for (int o = -4; o <= 4; ++o) {
+          if (4 + j + o < 0 || 4 + j + o > 11) continue;
+          k1 += T(kf[(o + 4) * 2]) * T(w[4 + j + o]);
+          k2 += T(kf[(o + 4) * 2 + 1]) * T(w[4 + j + o]);
+        }
+      }
+      g[j] -= T(F4(ua[dl], j)) * k1 + T(F4(ub[dl], j)) * k2;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) g[j] *= T(F4(c1, j));
+}
+
+template <int D, typename T, typename CF>
+__global__ void __launch_bounds__(kSmallThreads) k_schur_h_v4_lat(Geo G, const CF* __restrict__ cf, int crep,
+                                                                  const float* __restrict__ x,
+                                                                  T* __restrict__ hout, const int* act,
+                                                                  unsigned long long* pts) {
+  MPDE_PDL_ENTRY();
+  constexpr int NC = 2 + 2 * D;
+  const int v = blockIdx.y, P = G.P, pde = v / crep;
+  if (act && !act[pde]) return;
+  const int nl = G.n[D - 1];
+  if (pts && threadIdx.x == 0)
+    atomicAdd(pts, (unsigned long long)block_points(0, P, nl, blockIdx.x * blockDim.x * 4));
+  const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (p0 >= P) return;
+  int idx[D];
+  unravel<D>(G, p0, idx);
+  T g[4];
+  schur_h4_lat<D, T, CF>(G, cf + (size_t)pde * NC * P, x + (size_t)v * P, p0, idx, g);
+  stT4<T>(hout + (size_t)v * P + p0, g);
 }
 
 template <int D, typename T, typename CF = float>
@@ -1866,7 +1986,6 @@ static inline bool use_v4(const Geo& G) {
 }
 // small levels (<= 16384 points per vector): 4-points-per-thread kernels in 64-thread CTAs
 // (a 256-thread CTA per PDE leaves most SMs idle at the coarse levels)
-constexpr int kSmallThreads = 64;
 static int g_small_p = -1;  // points-per-vector threshold (env MPDE_SMALLP, default 16384)
 static inline bool small_level(const Geo& G) {
   if (g_small_p < 0) {
@@ -1876,6 +1995,14 @@ static inline bool small_level(const Geo& G) {
   return G.P <= g_small_p;
 }
 static inline int v4_threads(const Geo& G) { return small_level(G) ? kSmallThreads : kThreads; }
+static int g_small_lat = -1;  // env MPDE_SMALL_LAT=0: small-level pass 1 with the per-axis load phases
+static inline bool small_lat(const Geo& G) {
+  if (g_small_lat < 0) {
+    const char* e = getenv("MPDE_SMALL_LAT");
+    g_small_lat = e ? atoi(e) : 1;
+  }
+  return g_small_lat && small_level(G) && use_v4(G);
+}
 // warp-specialised interior / edge quads (remap_quad): NY4 a power of two dividing kThreads
 static int g_remap = -1;  // env MPDE_REMAP=1: warp-specialised interior / edge quad mapping
 static inline int use_remap(const Geo& G) {
@@ -2002,6 +2129,13 @@ void launch_schur_g(const Geo& G, int nvec, int crep, const float* cf, const flo
   if (use_v4(G)) {
     const int th = v4_threads(G);
     dim3 gr((G.P + 4 * th - 1) / (4 * th), nvec);
+    if (small_lat(G)) {  // latency-bound small level: all loads before the edge branches
+      if (f64)
+        DISPATCH_D2(G.D, k_schur_h_v4_lat<DD, double, float><<<gr, th, 0, s>>>(G, cf, crep, x, (double*)g, act, pts));
+      else
+        DISPATCH_D2(G.D, k_schur_h_v4_lat<DD, float, float><<<gr, th, 0, s>>>(G, cf, crep, x, (float*)g, act, pts));
+      return;
+    }
     if (f64)
       DISPATCH_D2(G.D, k_schur_h_v4<DD, double><<<gr, th, 0, s>>>(G, cf, crep, x, (double*)g, act, pts, 0));
     else
