@@ -175,8 +175,9 @@ def test_step_gradient_matches_central_differences(shape, h, bc):
     om = rng.normal(size=pr.P)
     om_n = rng.normal(size=(D, pr.P)) if bc is not None else None
     g = rng.normal(size=pr.n_v)
-    f = solve_forward(pr, c, b, om, method="dense", omega_n=om_n)
-    bw = solve_backward(pr, f, g, method="dense")
+    meth = "dense" if D == 2 else "lu"  # SuperLU + fp64 refinement: same accuracy, 3D in seconds
+    f = solve_forward(pr, c, b, om, method=meth, omega_n=om_n)
+    bw = solve_backward(pr, f, g, method=meth)
     gh = step_gradient(pr, f, bw)
     for d in range(D):
         eps = 1e-5 * h[d]
@@ -189,7 +190,7 @@ def test_step_gradient_matches_central_differences(shape, h, bc):
         Am, _, _ = assemble(prm, c, b, om, om_n)
         J = assemble_dh(pr, d, f["info"])
         assert abs((Ap - Am) / (2 * eps) - J).max() <= 1e-6 * abs(J).max()
-        lp = g @ solve_forward(prp, c, b, om, method="dense", omega_n=om_n)["z"]
-        lm = g @ solve_forward(prm, c, b, om, method="dense", omega_n=om_n)["z"]
+        lp = g @ solve_forward(prp, c, b, om, method=meth, omega_n=om_n)["z"]
+        lm = g @ solve_forward(prm, c, b, om, method=meth, omega_n=om_n)["z"]
         fd = (lp - lm) / (2 * eps)
         assert abs(fd - gh[d]) <= 1e-5 * max(abs(fd), abs(gh[d])), (d, fd, gh[d])
